@@ -1,0 +1,187 @@
+/*
+ * nnqs.h -- C-ABI of libnnqs: the local-energy hot path of NNQS-Transformer
+ * (arXiv 2306.16705) on NVIDIA B200 (sm_100a).
+ *
+ * Citations: "P:n" = PAPER.md line n (arXiv 2306.16705 LaTeX source).
+ *
+ * The path (Sec. 3.4; stages 2-4 of Sec. 3.2):
+ *   nnqs_ham_compress    Eq. (9) integrals -> JW Pauli table grouped by flip
+ *                        mask with fused coefficients (Fig. 6(c), Algorithm 1,
+ *                        P:309-363).  Host, once per molecule.
+ *   nnqs_table_prepare   the unique-sample lookup table ("bits of a
+ *                        64-bit integer ... two integers") + psi table (wf_lut,
+ *                        P:383).  Device.
+ *   nnqs_local_energy    E_loc(x) = sum_x' H_xx' psi(x')/psi(x), Eq. (4)
+ *                        (P:139-141), fused entry evaluation,
+ *                        sample-aware: x' not in the table contributes 0
+ *                        (P:379); Algorithm 2.  Device.
+ *   nnqs_energy_reduce   count-weighted mean and variance, Eq. (6)
+ *                        over unique samples with weights.  Device.
+ *
+ * Conventions:
+ *   - Spin orbital (p, s) of spatial orbital p, spin s (0 = alpha, 1 = beta) is
+ *     qubit 2p+s (0-indexed reading of P:287).  Occupied = bit 1.
+ *   - Configuration keys are uint64[2]: word0 = qubits 0..63, word1 = qubits
+ *     64..127; tables are strictly increasing as 128-bit integers
+ *     (compare word1, then word0).  N = n_spin_orbitals <= 128.
+ *   - Pauli table: H = sum_k sum_{i in group k} d_i X^{X_k} Z^{Z_i}, where
+ *     X^a Z^b flips the bits a after applying the sign (-1)^{popc(x & b)}; so
+ *     <x ^ X_k | H | x> = sum_i d_i (-1)^{popc(x & Z_i)}.  d_i is Algorithm 1's
+ *     fused coefficient c_i * Re((-i)^{Y_occ}) with the sign reading
+ *     R1 (Algorithm 2's literal "(sum & 1) ? 1 : -1", builds -H).
+ *   - log psi is complex, (Re, Im) interleaved float64; Re may be -inf (psi = 0).
+ *
+ * Memory: "host" / "device" is stated per pointer.  Device pointers are
+ * borrowed for the duration of a stream-ordered call only.  Handles own all
+ * their memory.  Every call returns a status; errors never abort the process.
+ * The message of the last error on the calling thread is nnqs_last_error().
+ */
+#ifndef NNQS_H
+#define NNQS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    NNQS_OK = 0,
+    NNQS_E_ARG = -1,       /* null / inconsistent argument */
+    NNQS_E_SIZE = -2,      /* N odd, N > 128, exact mode with N > 30, n < 0 */
+    NNQS_E_SYMMETRY = -3,  /* h1 not symmetric / h2 not 8-fold symmetric (1e-12 rel) */
+    NNQS_E_TABLE = -4,     /* keys not strictly increasing, rows out of range */
+    NNQS_E_ZERO_PSI = -5,  /* some row has psi(x) = 0: its E_loc is NaN, others valid */
+    NNQS_E_CUDA = -6,      /* CUDA runtime error */
+    NNQS_E_NOMEM = -7,     /* host or device allocation failed */
+    NNQS_E_EMPTY = -8,     /* sum of counts == 0 (Eq. 6 undefined) */
+    NNQS_E_ODD_Y = -9      /* Pauli input: odd-Y term with |Re c| > tol (SPEC reading) */
+};
+
+/* thread-local, static storage; "" if no error yet */
+const char *nnqs_last_error(void);
+/* library version / build string */
+const char *nnqs_version(void);
+
+typedef struct nnqs_ham_s *nnqs_ham;     /* immutable after creation; owns host + device copies */
+typedef struct nnqs_table_s *nnqs_table; /* owns its device copies; borrows nothing */
+
+/*
+ * nnqs_ham_compress -- Eq. (9) under Jordan-Wigner
+ * into the grouped table of Fig. 6(c) (Algorithm 1).
+ *   h1  host f64[n*n], row-major h_pq (n = n_spin_orbitals/2 spatial orbitals)
+ *   h2  host f64[n^4], chemists' (pq|rs) at ((p*n+q)*n+r)*n+s; the Eq. (9)
+ *       two-body term is 1/2 sum (pq|rs) a+_{ps} a+_{rt} a_{st} a_{qs}
+ *   e_core  constant (nuclear repulsion / frozen core) -> identity string
+ *   tol     drop strings with |d| <= tol (0 keeps every non-zero)
+ *   device  CUDA device ordinal that receives the device copy; device < 0
+ *           builds a host-only handle (info / export only, no CUDA calls)
+ * Validates symmetry (NNQS_E_SYMMETRY) and N (NNQS_E_SIZE).  Copies h1/h2; the
+ * caller keeps ownership.  Groups are ascending by 128-bit X, strings within a
+ * group ascending by Z.  The handle records that H conserves N_alpha and N_beta.
+ */
+int nnqs_ham_compress(const double *h1, const double *h2, int n_spin_orbitals, double e_core,
+                      double tol, int device, nnqs_ham *out);
+
+/*
+ * nnqs_ham_from_pauli -- Algorithm 1 on an explicit Pauli list
+ * (Fig. 6(a)): string i has X/Y mask xmask[i] (host u64[n][2]), Y/Z
+ * mask zmask[i] (host u64[n][2]) and complex coefficient (coeff_re, coeff_im)
+ * (host f64[n]); fused d = Re(c) * Re((-i)^{Y_occ}).  Duplicate strings are
+ * summed.  Odd Y_occ with |Re c| > tol -> NNQS_E_ODD_Y.  No sector assumption
+ * is recorded (every group is evaluated for every row).
+ */
+int nnqs_ham_from_pauli(const uint64_t *xmask, const uint64_t *zmask, const double *coeff_re,
+                        const double *coeff_im, int64_t n_terms, int n_qubits, double tol,
+                        int device, nnqs_ham *out);
+
+/* counts and device footprint (any pointer may be NULL) */
+int nnqs_ham_info(nnqs_ham h, int *n_qubits, int64_t *n_groups, int64_t *n_terms,
+                  int64_t *device_bytes);
+
+/*
+ * Export the grouped table to host buffers sized from nnqs_ham_info:
+ *   xmask u64[K][2], offsets i64[K+1] (offsets[0] = 0, CSR), zmask u64[Nh][2],
+ *   coeff f64[Nh] (fused d_i).  Any pointer may be NULL.
+ */
+int nnqs_ham_export(nnqs_ham h, uint64_t *xmask, int64_t *offsets, uint64_t *zmask, double *coeff);
+int nnqs_ham_free(nnqs_ham h);
+
+/*
+ * nnqs_table_prepare -- the lookup tables of Algorithm 2 (id_lut / wf_lut,
+ * P:383): validates strict 128-bit order, builds psi_hat(y) =
+ * exp(logpsi(y) - s), s = max Re logpsi, and a GF(2)-linear hash index over the
+ * keys (the lookup that replaces binary_find).
+ *   mode 0 (sample-aware): keys device u64[n][2] (sorted), logpsi device f64[n][2]
+ *   mode 1 (exact): keys == NULL, n = 2^N (N <= 30), logpsi indexed by configuration
+ *   cuda_stream  cudaStream_t (NULL = legacy default stream)
+ * Stream-ordered; returns NNQS_E_TABLE (after a stream sync) if the order check
+ * fails.
+ */
+int nnqs_table_prepare(nnqs_ham h, int mode, const uint64_t *keys, const double *logpsi,
+                       int64_t n, void *cuda_stream, nnqs_table *out);
+int nnqs_table_free(nnqs_table t);
+/* table size and the log-psi shift s (host out; may be NULL) */
+int nnqs_table_info(nnqs_table t, int64_t *n, double *shift, int64_t *device_bytes);
+
+/*
+ * nnqs_local_energy -- Eq. (4) for n_rows rows (Algorithm 2).
+ *   rows == NULL: the rows are table entries [row_begin, row_begin + n_rows)
+ *                 (the paper's ist / batch_size_cur_rank; in
+ *                 exact mode, the configurations row_begin...);
+ *   rows != NULL: explicit device u64[n_rows][2] with row_logpsi device
+ *                 f64[n_rows][2] (any configurations).
+ *   eloc_out  device f64[n_rows][2] = (Re, Im) E_loc
+ *   stats_out optional device i64[4] (zeroed by the caller) accumulating
+ *             (row-group pairs, pairs whose x' shares x's particle sector,
+ *              lookups that hit, Pauli strings evaluated); NULL to skip
+ * x' absent from the table contributes zero.  For Hamiltonians from
+ * nnqs_ham_compress, groups whose x' leaves x's (N_alpha, N_beta) sector are
+ * skipped (their exact H_xx' is 0).  A row with psi(x) = 0 gets NaN; this is
+ * reported by nnqs_local_energy_check().  Asynchronous on cuda_stream.
+ */
+int nnqs_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_t *rows,
+                      const double *row_logpsi, int64_t n_rows, double *eloc_out,
+                      int64_t *stats_out, void *cuda_stream);
+
+/* Synchronises cuda_stream; NNQS_E_ZERO_PSI if any of eloc (device f64[n][2]) is NaN. */
+int nnqs_local_energy_check(const double *eloc, int64_t n, void *cuda_stream);
+
+/*
+ * Energy reduction, Eq. (6) with weights:
+ *   mean = sum w E / W,  var = sum w |E - mean|^2 / W,  W = sum w  (two passes,
+ *   population variance).  Chunks of NNQS_REDUCE_CHUNK rows are reduced in a
+ *   fixed tree order and combined in ascending chunk order, so results are
+ *   bit-identical however the rows are split over devices (chunk-aligned).
+ *
+ * nnqs_energy_chunk_partials: partials device f64[n_chunks][3],
+ *   n_chunks = ceil(n / NNQS_REDUCE_CHUNK);  mean_dev == NULL: pass 1,
+ *   (W, sum w Re E, sum w Im E) per chunk;  mean_dev device f64[2]: pass 2,
+ *   (W, sum w |E - mean|^2, 0) per chunk.  eloc device f64[n][2], counts device i64[n].
+ * nnqs_energy_combine: partials device f64[n_chunks][3] -> out_dev device f64[4]:
+ *   pass 1: (mean_re, mean_im, W, 0);  pass 2: (var, W, 0, 0).
+ * nnqs_energy_reduce: single-device convenience, out host f64[4] =
+ *   (mean_re, mean_im, var, W); synchronises; NNQS_E_EMPTY if W == 0.
+ */
+#define NNQS_REDUCE_CHUNK 1024
+int nnqs_energy_chunk_partials(const double *eloc, const int64_t *counts, int64_t n,
+                               const double *mean_dev, double *partials, void *cuda_stream);
+int nnqs_energy_combine(const double *partials, int64_t n_chunks, int pass, double *out_dev,
+                        void *cuda_stream);
+int nnqs_energy_reduce(const double *eloc, const int64_t *counts, int64_t n, double out[4],
+                       void *cuda_stream);
+
+/*
+ * Parity/debug (small inputs): every (row, group) whose x' = x ^ X_k is found
+ * in the table, with its index and H_xx'.  rows: host u64[n_rows][2].  Outputs
+ * host arrays of capacity max_pairs; n_pairs_out = number found (may exceed
+ * max_pairs, then NNQS_E_SIZE).  Order unspecified.
+ */
+int nnqs_coupled_debug(nnqs_ham h, nnqs_table t, const uint64_t *rows_host, int64_t n_rows,
+                       int64_t max_pairs, int64_t *row_id, int64_t *group_id, uint64_t *xprime,
+                       int64_t *table_idx, double *h_xxp, int64_t *n_pairs_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NNQS_H */

@@ -213,11 +213,13 @@ int oracle_row_hits(int n, const double *h1, const double *h2, double e_core,
 /*
  * E_loc for n_rows rows (explicit keys + their log psi) against table T.
  * eloc_out [n_rows][2] = (Re, Im); NaN for a row with psi(x) = 0.
+ * scale_out (optional) [n_rows] = sum_x' |H_xx'| |psi(x')/psi(x)|, the scale of
+ * the parity tolerance (reading R14).
  */
 int oracle_eloc(int n, const double *h1, const double *h2, double e_core,
                 int exact, const uint64_t *keys, const double *logpsi, int64_t n_keys,
                 const uint64_t *rows, const double *row_logpsi, int64_t n_rows,
-                double *eloc_out, int n_threads) {
+                double *eloc_out, double *scale_out, int n_threads) {
     if (!exact && !check_sorted(keys, n_keys)) return -4;
     int rc = 0;
 #ifdef _OPENMP
@@ -239,11 +241,15 @@ int oracle_eloc(int n, const double *h1, const double *h2, double e_core,
         for (int64_t i = 0; i < n_rows; ++i) {
             if (!ok) continue;
             double lre = row_logpsi[2 * i], lim = row_logpsi[2 * i + 1];
-            if (isinf(lre) && lre < 0) { eloc_out[2 * i] = NAN; eloc_out[2 * i + 1] = NAN; continue; }
+            if (isinf(lre) && lre < 0) {
+                eloc_out[2 * i] = NAN; eloc_out[2 * i + 1] = NAN;
+                if (scale_out) scale_out[i] = NAN;
+                continue;
+            }
             det_t d = {{rows[2 * i], rows[2 * i + 1]}};
             apply_hamiltonian(n, h1, h2, e_core, &d, &c);
             qsort(c.list, (size_t)c.n_list, sizeof(int64_t), cmp_i64);
-            long double sr = 0, cr = 0, si = 0, ci = 0;
+            long double sr = 0, cr = 0, si = 0, ci = 0, sa = 0;
             for (int64_t t = 0; t < c.n_list; ++t) {
                 int64_t idx = c.list[t];
                 long double h = c.acc[idx];
@@ -251,7 +257,9 @@ int oracle_eloc(int n, const double *h1, const double *h2, double e_core,
                 long double ph = (long double)logpsi[2 * idx + 1] - (long double)lim;
                 neumaier(&sr, &cr, h * mag * cosl(ph));
                 neumaier(&si, &ci, h * mag * sinl(ph));
+                sa += fabsl(h) * mag;
             }
+            if (scale_out) scale_out[i] = (double)sa;
             eloc_out[2 * i] = (double)(sr + cr);
             eloc_out[2 * i + 1] = (double)(si + ci);
             ctx_reset(&c);

@@ -30,7 +30,7 @@ def lib():
                                       ctypes.c_int64, P, ctypes.c_int64, P, P, P]
         L.oracle_row_hits.restype = ctypes.c_int
         L.oracle_eloc.argtypes = [ctypes.c_int, P, P, ctypes.c_double, ctypes.c_int, P, P,
-                                  ctypes.c_int64, P, P, ctypes.c_int64, P, ctypes.c_int]
+                                  ctypes.c_int64, P, P, ctypes.c_int64, P, P, ctypes.c_int]
         L.oracle_eloc.restype = ctypes.c_int
         L.oracle_num_threads.restype = ctypes.c_int
         _lib = L
@@ -71,9 +71,10 @@ def row_hits(h1, h2, e_core, x, keys=None, n_qubits=None, max_hits=1 << 22):
     return idx[: nh[0]].copy(), hv[: nh[0]].copy()
 
 
-def eloc(h1, h2, e_core, rows, row_logpsi, keys=None, logpsi=None, n_threads=0):
+def eloc(h1, h2, e_core, rows, row_logpsi, keys=None, logpsi=None, n_threads=0, with_scale=False):
     """E_loc (Eq. 4) for explicit rows.  keys=None -> exact mode with logpsi
-    indexed by configuration.  Returns complex128 [n_rows]."""
+    indexed by configuration.  Returns complex128 [n_rows] (and, with
+    with_scale, the per-row tolerance scale sum |H_xx'| |psi(x')/psi(x)|)."""
     h1, h2, n = _ints(h1, h2)
     rows = np.ascontiguousarray(rows, dtype=np.uint64).reshape(-1, 2)
     row_logpsi = np.ascontiguousarray(row_logpsi, dtype=np.float64).reshape(-1, 2)
@@ -86,11 +87,13 @@ def eloc(h1, h2, e_core, rows, row_logpsi, keys=None, logpsi=None, n_threads=0):
         kp, n_keys = _p(keys), len(keys)
         assert len(logpsi) == n_keys
     out = np.empty((len(rows), 2), dtype=np.float64)
+    scale = np.empty(len(rows), dtype=np.float64)
     rc = lib().oracle_eloc(n, _p(h1), _p(h2), float(e_core), int(exact), kp, _p(logpsi), n_keys,
-                           _p(rows), _p(row_logpsi), len(rows), _p(out), int(n_threads))
+                           _p(rows), _p(row_logpsi), len(rows), _p(out), _p(scale), int(n_threads))
     if rc != 0:
         raise RuntimeError(f"oracle_eloc failed: {rc}")
-    return out[:, 0] + 1j * out[:, 1]
+    e = out[:, 0] + 1j * out[:, 1]
+    return (e, scale) if with_scale else e
 
 
 def num_threads() -> int:

@@ -1,0 +1,88 @@
+// Internal declarations of libnnqs (not part of the C-ABI; see include/nnqs.h).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/nnqs.h"
+
+typedef unsigned long long u64;
+
+// ----------------------------------------------------------------- errors
+int nnqs_set_error(int code, const std::string &msg);
+
+// ---------------------------------------------------------- GF(2) hash
+// h(x) = XOR_{j : bit j of x set} col[j]: linear over GF(2), so
+// h(x ^ X) = h(x) ^ h(X) and one XOR per (row, group) gives the bucket
+// of x' = x ^ X_k.  Columns come from splitmix64 with a fixed seed.
+static inline u64 nnqs_splitmix64(u64 &s) {
+    u64 z = (s += 0x9E3779B97F4A7C15ULL);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+void nnqs_hash_columns(u64 cols[128]);
+u64 nnqs_hash_host(const u64 cols[128], u64 lo, u64 hi);
+
+// ------------------------------------------------------------ Hamiltonian
+struct HostTable {
+    int n_qubits = 0;
+    bool conserving = false;          // H conserves N_alpha and N_beta (compress)
+    std::vector<u64> x;               // [K][2]
+    std::vector<int64_t> off;         // [K+1]
+    std::vector<u64> z;               // [Nh][2]
+    std::vector<double> d;            // [Nh]
+};
+
+// host compress (compress.cpp): Eq. (9) -> grouped fused Pauli table
+int nnqs_compress_host(const double *h1, const double *h2, int n, double e_core, double tol,
+                       HostTable &out);
+int nnqs_from_pauli_host(const u64 *xm, const u64 *zm, const double *cre, const double *cim,
+                         int64_t n_terms, int n_qubits, double tol, HostTable &out);
+
+struct DeviceHam {
+    // group arrays [K]
+    void *gx = nullptr;       // ulonglong2 X mask
+    u64 *ghx = nullptr;       // h(X)
+    uint32_t *ginfo = nullptr;// bits 0..7: popc(X & alpha)/2, 8..15: popc(X & beta)/2
+    uint32_t *goff = nullptr; // [K+1] term offsets
+    // term arrays [Nh]
+    void *tz = nullptr;       // ulonglong2 Z mask
+    double *td = nullptr;     // fused coefficient d
+    int64_t bytes = 0;
+};
+
+struct nnqs_ham_s {
+    HostTable host;
+    DeviceHam dev;
+    int device = 0;
+    int64_t n_groups = 0, n_terms = 0;
+};
+
+struct nnqs_table_s {
+    int mode = 0;             // 0 sample-aware, 1 exact
+    int device = 0;
+    int64_t n = 0;
+    void *stream = nullptr;
+    void *keys = nullptr;     // ulonglong2 [n] (mode 0)
+    void *logpsi = nullptr;   // double2 [n]
+    void *psi_hat = nullptr;  // double2 [n]
+    u64 *slots = nullptr;     // hash slots [4 * n_buckets] (mode 0)
+    u64 bucket_mask = 0;
+    u64 *shift_key = nullptr; // device: order-preserving key of s = max Re logpsi
+    int *flag = nullptr;      // device: order violation flag
+    int64_t bytes = 0;
+};
+
+// device side (kernels.cu)
+int nnqs_ham_upload(nnqs_ham h);
+void nnqs_ham_release(nnqs_ham h);
+int nnqs_table_build(nnqs_table t, const uint64_t *keys, const double *logpsi, void *stream);
+void nnqs_table_release(nnqs_table t);
+int nnqs_launch_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_t *rows,
+                             const double *row_logpsi, int64_t n_rows, double *eloc,
+                             int64_t *stats, void *stream);
+int nnqs_launch_coupled_debug(nnqs_ham h, nnqs_table t, const uint64_t *rows_dev, int64_t n_rows,
+                              int64_t max_pairs, int64_t *out_i64 /*[max][3]*/, u64 *out_x /*[max][2]*/,
+                              double *out_h, unsigned long long *counter, void *stream);

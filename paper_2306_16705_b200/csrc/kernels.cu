@@ -1,0 +1,599 @@
+// kernels.cu -- device side of libnnqs (sm_100a).
+//
+//   table build      id_lut / wf_lut of Algorithm 2: order check,
+//                    psi_hat = exp(logpsi - s), GF(2)-linear hash index
+//   local energy     Eq. (4) over the grouped table of Fig. 6(c),
+//                    fused entry evaluation + sample-aware lookup
+//                    (PAPER.md:379-381); Algorithm 2
+//   energy reduce    Eq. (6) with counts
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+
+#include "internal.h"
+
+#define NNQS_EMPTY_SLOT 0xFFFFFFFFFFFFFFFFULL
+#define ALPHA_MASK 0x5555555555555555ULL
+#define BETA_MASK 0xAAAAAAAAAAAAAAAAULL
+
+__constant__ u64 c_hash[128];
+
+namespace {
+
+bool g_hash_ready[64] = {false};
+
+int ensure_hash(int device) {
+    if (device < 0 || device >= 64) return NNQS_E_ARG;
+    if (g_hash_ready[device]) return NNQS_OK;
+    u64 cols[128];
+    nnqs_hash_columns(cols);
+    cudaError_t e = cudaMemcpyToSymbol(c_hash, cols, sizeof(cols));
+    if (e != cudaSuccess) return nnqs_set_error(NNQS_E_CUDA, cudaGetErrorString(e));
+    g_hash_ready[device] = true;
+    return NNQS_OK;
+}
+
+inline int cuda_check(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return NNQS_OK;
+    return nnqs_set_error(e == cudaErrorMemoryAllocation ? NNQS_E_NOMEM : NNQS_E_CUDA,
+                          std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct HamView {
+    const ulonglong2 *gx;
+    const u64 *ghx;
+    const uint32_t *ginfo;
+    const uint32_t *goff;
+    const ulonglong2 *tz;
+    const double *td;
+    int64_t K;
+};
+
+struct TabView {
+    int64_t n;
+    const ulonglong2 *keys;
+    const double2 *logpsi;
+    const double2 *psi_hat;
+    const u64 *slots;
+    u64 bucket_mask;
+    const u64 *shift_key;
+};
+
+HamView ham_view(nnqs_ham h) {
+    return {(const ulonglong2 *)h->dev.gx, h->dev.ghx, h->dev.ginfo, h->dev.goff,
+            (const ulonglong2 *)h->dev.tz, h->dev.td, h->n_groups};
+}
+
+TabView tab_view(nnqs_table t) {
+    return {t->n, (const ulonglong2 *)t->keys, (const double2 *)t->logpsi,
+            (const double2 *)t->psi_hat, t->slots, t->bucket_mask, t->shift_key};
+}
+
+// ------------------------------------------------------------ device helpers
+__device__ __forceinline__ u64 hash128(u64 lo, u64 hi) {
+    u64 h = 0;
+    while (lo) {
+        h ^= c_hash[__ffsll((long long)lo) - 1];
+        lo &= lo - 1;
+    }
+    while (hi) {
+        h ^= c_hash[64 + __ffsll((long long)hi) - 1];
+        hi &= hi - 1;
+    }
+    return h;
+}
+
+// order-preserving map double -> u64 (for atomicMax)
+__device__ __forceinline__ u64 dkey(double v) {
+    u64 b = (u64)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double dkey_inv(u64 k) {
+    if (k == 0) return 0.0;                       // no finite entry
+    u64 b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFULL) : ~k;
+    return __longlong_as_double((long long)b);
+}
+
+// bucketised linear probing: 4 slots (32 B) per bucket, slot = fp32 << 32 | rank
+__device__ __forceinline__ int64_t probe(const TabView &T, u64 h, u64 p0, u64 p1) {
+    u64 b = h & T.bucket_mask;
+    const uint32_t fp = (uint32_t)(h >> 32);
+    while (true) {
+        const ulonglong2 *bk = reinterpret_cast<const ulonglong2 *>(T.slots + 4 * b);
+        const ulonglong2 s01 = __ldg(bk), s23 = __ldg(bk + 1);
+        const u64 s[4] = {s01.x, s01.y, s23.x, s23.y};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (s[i] == NNQS_EMPTY_SLOT) return -1;
+            if ((uint32_t)(s[i] >> 32) == fp) {
+                const uint32_t r = (uint32_t)s[i];
+                const ulonglong2 k = __ldg(T.keys + r);
+                if (k.x == p0 && k.y == p1) return (int64_t)r;
+            }
+        }
+        b = (b + 1) & T.bucket_mask;
+    }
+}
+
+__device__ __forceinline__ double flip_sign(double d, int parity) {
+    return __longlong_as_double(__double_as_longlong(d) ^ ((long long)parity << 63));
+}
+
+// H_{x', x} = sum_{i in group k} d_i (-1)^{popc(x & Z_i)}   (reading R1/R2)
+__device__ __forceinline__ double group_value(const HamView &H, int64_t k, u64 x0, u64 x1,
+                                              u64 &n_str) {
+    const uint32_t b = __ldg(H.goff + k), e = __ldg(H.goff + k + 1);
+    double hv = 0.0;
+    for (uint32_t i = b; i < e; ++i) {
+        const ulonglong2 Z = __ldg(H.tz + i);
+        const int par = (__popcll(x0 & Z.x) + __popcll(x1 & Z.y)) & 1;
+        hv += flip_sign(__ldg(H.td + i), par);
+    }
+    n_str += e - b;
+    return hv;
+}
+
+// ------------------------------------------------------------ table build
+__global__ void k_check_order(const ulonglong2 *keys, int64_t n, int *flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + 1; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const ulonglong2 a = keys[i - 1], b = keys[i];
+        if (!(a.y < b.y || (a.y == b.y && a.x < b.x))) atomicOr(flag, 1);
+    }
+}
+
+__global__ void k_max_re(const double2 *lp, int64_t n, u64 *shift_key) {
+    u64 m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = lp[i].x;
+        if (isfinite(v)) m = max(m, dkey(v));
+    }
+    for (int o = 16; o; o >>= 1) m = max(m, (u64)__shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax((unsigned long long *)shift_key, (unsigned long long)m);
+}
+
+__global__ void k_psi_hat(const double2 *lp, int64_t n, const u64 *shift_key, double2 *ph) {
+    const double s = dkey_inv(*shift_key);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 l = lp[i];
+        const double m = exp(l.x - s);
+        double sn, cs;
+        sincos(l.y, &sn, &cs);
+        ph[i] = make_double2(m * cs, m * sn);
+    }
+}
+
+__global__ void k_hash_insert(const ulonglong2 *keys, int64_t n, u64 *slots, u64 mask) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const ulonglong2 k = keys[i];
+        const u64 h = hash128(k.x, k.y);
+        const u64 val = ((h >> 32) << 32) | (u64)(uint32_t)i;
+        u64 b = h & mask;
+        bool done = false;
+        while (!done) {
+            for (int s = 0; s < 4 && !done; ++s) {
+                const u64 old = atomicCAS((unsigned long long *)(slots + 4 * b + s),
+                                          (unsigned long long)NNQS_EMPTY_SLOT, (unsigned long long)val);
+                done = old == NNQS_EMPTY_SLOT;
+            }
+            b = (b + 1) & mask;
+        }
+    }
+}
+
+// ------------------------------------------------------------ local energy
+// v1: one thread per row, grid-stride over rows, groups in
+// ascending order, per-row accumulation order = ascending k.
+template <int MODE, bool CONS>
+__global__ void __launch_bounds__(256) k_eloc_v1(HamView H, TabView T, int64_t row_begin,
+                                                 const ulonglong2 *rows, const double2 *row_lp,
+                                                 int64_t n_rows, double2 *out,
+                                                 unsigned long long *stats) {
+    const double s = dkey_inv(*T.shift_key);
+    u64 c_pairs = 0, c_sec = 0, c_hit = 0, c_str = 0;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        u64 x0, x1;
+        double2 lx;
+        if (rows) {
+            const ulonglong2 k = rows[r];
+            x0 = k.x; x1 = k.y;
+            lx = row_lp[r];
+        } else {
+            const int64_t i = row_begin + r;
+            if (MODE == 0) {
+                const ulonglong2 k = T.keys[i];
+                x0 = k.x; x1 = k.y;
+            } else {
+                x0 = (u64)i; x1 = 0;
+            }
+            lx = T.logpsi[i];
+        }
+        if (!(lx.x > -INFINITY)) {                 // psi(x) = 0: 0/0 (reading R10)
+            out[r] = make_double2(NAN, NAN);
+            continue;
+        }
+        const double rel = lx.x - s;
+        const bool direct = rel < -600.0;          // reading R11 fallback
+        const u64 hx = (MODE == 0) ? hash128(x0, x1) : 0;
+        double ar = 0.0, ai = 0.0;
+        for (int64_t k = 0; k < H.K; ++k) {
+            const ulonglong2 X = __ldg(H.gx + k);
+            if (CONS) {
+                const uint32_t info = __ldg(H.ginfo + k);
+                const int na = __popcll(x0 & X.x & ALPHA_MASK) + __popcll(x1 & X.y & ALPHA_MASK);
+                const int nb = __popcll(x0 & X.x & BETA_MASK) + __popcll(x1 & X.y & BETA_MASK);
+                if (na != (int)(info & 0xff) || nb != (int)((info >> 8) & 0xff)) continue;
+            }
+            ++c_sec;
+            const u64 p0 = x0 ^ X.x, p1 = x1 ^ X.y;
+            int64_t idx;
+            if (MODE == 1) idx = (p1 == 0 && p0 < (u64)T.n) ? (int64_t)p0 : -1;
+            else idx = probe(T, hx ^ __ldg(H.ghx + k), p0, p1);
+            if (idx < 0) continue;
+            ++c_hit;
+            const double hv = group_value(H, k, x0, x1, c_str);
+            double2 ps;
+            if (!direct) {
+                ps = __ldg(T.psi_hat + idx);
+            } else {
+                const double2 l = T.logpsi[idx];
+                const double m = exp(l.x - lx.x);
+                double sn, cs;
+                sincos(l.y - lx.y, &sn, &cs);
+                ps = make_double2(m * cs, m * sn);
+            }
+            ar = fma(hv, ps.x, ar);
+            ai = fma(hv, ps.y, ai);
+        }
+        c_pairs += (u64)H.K;
+        double2 e;
+        if (direct) {
+            e = make_double2(ar, ai);
+        } else {
+            // E = acc / psi_hat(x) = acc * exp(-(logpsi(x) - s))
+            const double m = exp(-rel);
+            double sn, cs;
+            sincos(-lx.y, &sn, &cs);
+            const double ir = m * cs, ii = m * sn;
+            e = make_double2(ar * ir - ai * ii, ar * ii + ai * ir);
+        }
+        out[r] = e;
+    }
+    if (stats) {
+        for (int o = 16; o; o >>= 1) {
+            c_pairs += __shfl_xor_sync(0xffffffffu, c_pairs, o);
+            c_sec += __shfl_xor_sync(0xffffffffu, c_sec, o);
+            c_hit += __shfl_xor_sync(0xffffffffu, c_hit, o);
+            c_str += __shfl_xor_sync(0xffffffffu, c_str, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(stats + 0, c_pairs);
+            atomicAdd(stats + 1, c_sec);
+            atomicAdd(stats + 2, c_hit);
+            atomicAdd(stats + 3, c_str);
+        }
+    }
+}
+
+template <int MODE, bool CONS>
+__global__ void k_coupled_debug(HamView H, TabView T, const ulonglong2 *rows, int64_t n_rows,
+                                int64_t max_pairs, int64_t *oi, u64 *ox, double *oh,
+                                unsigned long long *counter) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const u64 x0 = rows[r].x, x1 = rows[r].y;
+        const u64 hx = (MODE == 0) ? hash128(x0, x1) : 0;
+        u64 dummy = 0;
+        for (int64_t k = 0; k < H.K; ++k) {
+            const ulonglong2 X = H.gx[k];
+            if (CONS) {
+                const uint32_t info = H.ginfo[k];
+                const int na = __popcll(x0 & X.x & ALPHA_MASK) + __popcll(x1 & X.y & ALPHA_MASK);
+                const int nb = __popcll(x0 & X.x & BETA_MASK) + __popcll(x1 & X.y & BETA_MASK);
+                if (na != (int)(info & 0xff) || nb != (int)((info >> 8) & 0xff)) continue;
+            }
+            const u64 p0 = x0 ^ X.x, p1 = x1 ^ X.y;
+            int64_t idx;
+            if (MODE == 1) idx = (p1 == 0 && p0 < (u64)T.n) ? (int64_t)p0 : -1;
+            else idx = probe(T, hx ^ H.ghx[k], p0, p1);
+            if (idx < 0) continue;
+            const double hv = group_value(H, k, x0, x1, dummy);
+            const unsigned long long slot = atomicAdd(counter, 1ULL);
+            if ((int64_t)slot < max_pairs) {
+                oi[3 * slot] = r;
+                oi[3 * slot + 1] = k;
+                oi[3 * slot + 2] = idx;
+                ox[2 * slot] = p0;
+                ox[2 * slot + 1] = p1;
+                oh[slot] = hv;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------ energy reduce
+// one 256-thread block per chunk of NNQS_REDUCE_CHUNK rows; fixed tree order
+__global__ void __launch_bounds__(256) k_chunk_partials(const double2 *eloc, const int64_t *counts,
+                                                        int64_t n, const double *mean,
+                                                        double *partials) {
+    __shared__ double sa[256], sb[256], sc[256];
+    const int64_t base = (int64_t)blockIdx.x * NNQS_REDUCE_CHUNK;
+    double a = 0.0, b = 0.0, c = 0.0;
+    double mr = 0.0, mi = 0.0;
+    if (mean) { mr = mean[0]; mi = mean[1]; }
+    for (int j = 0; j < NNQS_REDUCE_CHUNK / 256; ++j) {
+        const int64_t i = base + threadIdx.x + 256 * j;
+        if (i < n) {
+            const double w = (double)counts[i];
+            const double2 e = eloc[i];
+            a += w;
+            if (!mean) {
+                b = fma(w, e.x, b);
+                c = fma(w, e.y, c);
+            } else {
+                const double dr = e.x - mr, di = e.y - mi;
+                b = fma(w, dr * dr + di * di, b);
+            }
+        }
+    }
+    sa[threadIdx.x] = a; sb[threadIdx.x] = b; sc[threadIdx.x] = c;
+    __syncthreads();
+    for (int s = 128; s; s >>= 1) {
+        if (threadIdx.x < s) {
+            sa[threadIdx.x] += sa[threadIdx.x + s];
+            sb[threadIdx.x] += sb[threadIdx.x + s];
+            sc[threadIdx.x] += sc[threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        partials[3 * blockIdx.x] = sa[0];
+        partials[3 * blockIdx.x + 1] = sb[0];
+        partials[3 * blockIdx.x + 2] = sc[0];
+    }
+}
+
+__global__ void k_combine(const double *partials, int64_t n_chunks, int pass, double *out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double W = 0.0, S1 = 0.0, S2 = 0.0;
+    for (int64_t c = 0; c < n_chunks; ++c) {     // ascending chunk order
+        W += partials[3 * c];
+        S1 += partials[3 * c + 1];
+        S2 += partials[3 * c + 2];
+    }
+    if (pass == 1) {
+        out[0] = S1 / W; out[1] = S2 / W; out[2] = W; out[3] = 0.0;
+    } else {
+        out[0] = S1 / W; out[1] = W; out[2] = 0.0; out[3] = 0.0;
+    }
+}
+
+__global__ void k_any_nan(const double *x, int64_t n, int *flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (isnan(x[i])) atomicOr(flag, 1);
+}
+
+inline int grid_for(int64_t n, int block) {
+    int64_t g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > 148 * 16) g = 148 * 16;
+    return (int)g;
+}
+
+}  // namespace
+
+// ======================================================================= host
+int nnqs_ham_upload(nnqs_ham h) {
+    int rc = ensure_hash(h->device);
+    if (rc) return rc;
+    const HostTable &H = h->host;
+    const int64_t K = (int64_t)H.off.size() - 1, Nh = (int64_t)H.d.size();
+    if (Nh >= (int64_t)0xFFFFFFFFLL)
+        return nnqs_set_error(NNQS_E_SIZE, "more than 2^32-1 Pauli strings");
+    u64 cols[128];
+    nnqs_hash_columns(cols);
+    std::vector<u64> hx(K);
+    std::vector<uint32_t> info(K), off(K + 1);
+    for (int64_t k = 0; k < K; ++k) {
+        const u64 x0 = H.x[2 * k], x1 = H.x[2 * k + 1];
+        hx[k] = nnqs_hash_host(cols, x0, x1);
+        const int na = __builtin_popcountll(x0 & ALPHA_MASK) + __builtin_popcountll(x1 & ALPHA_MASK);
+        const int nb = __builtin_popcountll(x0 & BETA_MASK) + __builtin_popcountll(x1 & BETA_MASK);
+        info[k] = (uint32_t)(na / 2) | ((uint32_t)(nb / 2) << 8) | ((uint32_t)((na & 1) | (nb & 1)) << 16);
+        off[k] = (uint32_t)H.off[k];
+    }
+    off[K] = (uint32_t)H.off[K];
+    DeviceHam &D = h->dev;
+    size_t bx = 16 * (size_t)K, bh = 8 * (size_t)K, bi = 4 * (size_t)K, bo = 4 * (size_t)(K + 1),
+           bz = 16 * (size_t)Nh, bd = 8 * (size_t)Nh;
+    if ((rc = cuda_check(cudaMalloc(&D.gx, bx ? bx : 16), "cudaMalloc gx"))) return rc;
+    if ((rc = cuda_check(cudaMalloc((void **)&D.ghx, bh ? bh : 8), "cudaMalloc ghx"))) return rc;
+    if ((rc = cuda_check(cudaMalloc((void **)&D.ginfo, bi ? bi : 4), "cudaMalloc ginfo"))) return rc;
+    if ((rc = cuda_check(cudaMalloc((void **)&D.goff, bo), "cudaMalloc goff"))) return rc;
+    if ((rc = cuda_check(cudaMalloc(&D.tz, bz ? bz : 16), "cudaMalloc tz"))) return rc;
+    if ((rc = cuda_check(cudaMalloc((void **)&D.td, bd ? bd : 8), "cudaMalloc td"))) return rc;
+    if (K) {
+        if ((rc = cuda_check(cudaMemcpy(D.gx, H.x.data(), bx, cudaMemcpyHostToDevice), "copy gx"))) return rc;
+        if ((rc = cuda_check(cudaMemcpy(D.ghx, hx.data(), bh, cudaMemcpyHostToDevice), "copy ghx"))) return rc;
+        if ((rc = cuda_check(cudaMemcpy(D.ginfo, info.data(), bi, cudaMemcpyHostToDevice), "copy ginfo"))) return rc;
+    }
+    if ((rc = cuda_check(cudaMemcpy(D.goff, off.data(), bo, cudaMemcpyHostToDevice), "copy goff"))) return rc;
+    if (Nh) {
+        if ((rc = cuda_check(cudaMemcpy(D.tz, H.z.data(), bz, cudaMemcpyHostToDevice), "copy tz"))) return rc;
+        if ((rc = cuda_check(cudaMemcpy(D.td, H.d.data(), bd, cudaMemcpyHostToDevice), "copy td"))) return rc;
+    }
+    D.bytes = (int64_t)(bx + bh + bi + bo + bz + bd);
+    return NNQS_OK;
+}
+
+void nnqs_ham_release(nnqs_ham h) {
+    DeviceHam &D = h->dev;
+    cudaFree(D.gx); cudaFree(D.ghx); cudaFree(D.ginfo); cudaFree(D.goff); cudaFree(D.tz); cudaFree(D.td);
+    D = DeviceHam();
+}
+
+int nnqs_table_build(nnqs_table t, const uint64_t *keys, const double *logpsi, void *stream) {
+    int rc = ensure_hash(t->device);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = t->n;
+    size_t bk = 16 * (size_t)n;
+    // shift key + flag in one small allocation
+    if ((rc = cuda_check(cudaMallocAsync((void **)&t->shift_key, 16, st), "alloc shift"))) return rc;
+    t->flag = (int *)(t->shift_key + 1);
+    if ((rc = cuda_check(cudaMemsetAsync(t->shift_key, 0, 16, st), "memset shift"))) return rc;
+    if ((rc = cuda_check(cudaMallocAsync(&t->logpsi, bk ? bk : 16, st), "alloc logpsi"))) return rc;
+    if ((rc = cuda_check(cudaMallocAsync(&t->psi_hat, bk ? bk : 16, st), "alloc psi_hat"))) return rc;
+    if (n) {
+        if ((rc = cuda_check(cudaMemcpyAsync(t->logpsi, logpsi, bk, cudaMemcpyDeviceToDevice, st), "copy logpsi"))) return rc;
+    }
+    t->bytes = 16 + 2 * (int64_t)bk;
+    if (t->mode == 0) {
+        u64 nb = 1;
+        while (nb * 4 < 2 * (u64)(n > 0 ? n : 1)) nb <<= 1;   // load factor <= 1/2
+        t->bucket_mask = nb - 1;
+        if ((rc = cuda_check(cudaMallocAsync(&t->keys, bk ? bk : 16, st), "alloc keys"))) return rc;
+        if ((rc = cuda_check(cudaMallocAsync((void **)&t->slots, 32 * nb, st), "alloc slots"))) return rc;
+        if (n) {
+            if ((rc = cuda_check(cudaMemcpyAsync(t->keys, keys, bk, cudaMemcpyDeviceToDevice, st), "copy keys"))) return rc;
+        }
+        if ((rc = cuda_check(cudaMemsetAsync(t->slots, 0xFF, 32 * nb, st), "memset slots"))) return rc;
+        t->bytes += (int64_t)bk + 32 * (int64_t)nb;
+        if (n > 1) k_check_order<<<grid_for(n, 256), 256, 0, st>>>((const ulonglong2 *)t->keys, n, t->flag);
+        if (n) k_hash_insert<<<grid_for(n, 256), 256, 0, st>>>((const ulonglong2 *)t->keys, n, t->slots, t->bucket_mask);
+    }
+    if (n) {
+        k_max_re<<<grid_for(n, 256), 256, 0, st>>>((const double2 *)t->logpsi, n, t->shift_key);
+        k_psi_hat<<<grid_for(n, 256), 256, 0, st>>>((const double2 *)t->logpsi, n, t->shift_key,
+                                                     (double2 *)t->psi_hat);
+    }
+    if ((rc = cuda_check(cudaGetLastError(), "table kernels"))) return rc;
+    if (t->mode == 0 && n > 1) {
+        int flag = 0;
+        if ((rc = cuda_check(cudaMemcpyAsync(&flag, t->flag, sizeof(int), cudaMemcpyDeviceToHost, st), "read flag"))) return rc;
+        if ((rc = cuda_check(cudaStreamSynchronize(st), "sync"))) return rc;
+        if (flag) return nnqs_set_error(NNQS_E_TABLE, "keys are not strictly increasing as 128-bit integers");
+    }
+    return NNQS_OK;
+}
+
+void nnqs_table_release(nnqs_table t) {
+    cudaStream_t st = (cudaStream_t)t->stream;
+    if (t->keys) cudaFreeAsync(t->keys, st);
+    if (t->logpsi) cudaFreeAsync(t->logpsi, st);
+    if (t->psi_hat) cudaFreeAsync(t->psi_hat, st);
+    if (t->slots) cudaFreeAsync(t->slots, st);
+    if (t->shift_key) cudaFreeAsync(t->shift_key, st);
+    t->keys = t->logpsi = t->psi_hat = nullptr;
+    t->slots = t->shift_key = nullptr;
+}
+
+int nnqs_launch_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_t *rows,
+                             const double *row_logpsi, int64_t n_rows, double *eloc,
+                             int64_t *stats, void *stream) {
+    if (n_rows == 0) return NNQS_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    HamView H = ham_view(h);
+    TabView T = tab_view(t);
+    const bool cons = h->host.conserving;
+    const int g = grid_for(n_rows, 256);
+    auto *r = (const ulonglong2 *)rows;
+    auto *rl = (const double2 *)row_logpsi;
+    auto *o = (double2 *)eloc;
+    auto *s = (unsigned long long *)stats;
+    if (t->mode == 0) {
+        if (cons) k_eloc_v1<0, true><<<g, 256, 0, st>>>(H, T, row_begin, r, rl, n_rows, o, s);
+        else k_eloc_v1<0, false><<<g, 256, 0, st>>>(H, T, row_begin, r, rl, n_rows, o, s);
+    } else {
+        if (cons) k_eloc_v1<1, true><<<g, 256, 0, st>>>(H, T, row_begin, r, rl, n_rows, o, s);
+        else k_eloc_v1<1, false><<<g, 256, 0, st>>>(H, T, row_begin, r, rl, n_rows, o, s);
+    }
+    return cuda_check(cudaGetLastError(), "local energy launch");
+}
+
+int nnqs_launch_coupled_debug(nnqs_ham h, nnqs_table t, const uint64_t *rows_dev, int64_t n_rows,
+                              int64_t max_pairs, int64_t *oi, u64 *ox, double *oh,
+                              unsigned long long *counter, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    HamView H = ham_view(h);
+    TabView T = tab_view(t);
+    const bool cons = h->host.conserving;
+    const int g = grid_for(n_rows, 128);
+    auto *r = (const ulonglong2 *)rows_dev;
+    if (t->mode == 0) {
+        if (cons) k_coupled_debug<0, true><<<g, 128, 0, st>>>(H, T, r, n_rows, max_pairs, oi, ox, oh, counter);
+        else k_coupled_debug<0, false><<<g, 128, 0, st>>>(H, T, r, n_rows, max_pairs, oi, ox, oh, counter);
+    } else {
+        if (cons) k_coupled_debug<1, true><<<g, 128, 0, st>>>(H, T, r, n_rows, max_pairs, oi, ox, oh, counter);
+        else k_coupled_debug<1, false><<<g, 128, 0, st>>>(H, T, r, n_rows, max_pairs, oi, ox, oh, counter);
+    }
+    return cuda_check(cudaGetLastError(), "coupled debug launch");
+}
+
+// ----------------------------------------------------------- C-ABI: reduce
+extern "C" int nnqs_energy_chunk_partials(const double *eloc, const int64_t *counts, int64_t n,
+                                          const double *mean_dev, double *partials,
+                                          void *cuda_stream) {
+    if (n < 0 || (n > 0 && (!eloc || !counts || !partials)))
+        return nnqs_set_error(NNQS_E_ARG, "nnqs_energy_chunk_partials: bad arguments");
+    if (n == 0) return NNQS_OK;
+    const int64_t chunks = (n + NNQS_REDUCE_CHUNK - 1) / NNQS_REDUCE_CHUNK;
+    k_chunk_partials<<<(unsigned)chunks, 256, 0, (cudaStream_t)cuda_stream>>>(
+        (const double2 *)eloc, counts, n, mean_dev, partials);
+    return cuda_check(cudaGetLastError(), "chunk partials launch");
+}
+
+extern "C" int nnqs_energy_combine(const double *partials, int64_t n_chunks, int pass,
+                                   double *out_dev, void *cuda_stream) {
+    if (!partials || !out_dev || n_chunks <= 0 || (pass != 1 && pass != 2))
+        return nnqs_set_error(NNQS_E_ARG, "nnqs_energy_combine: bad arguments");
+    k_combine<<<1, 32, 0, (cudaStream_t)cuda_stream>>>(partials, n_chunks, pass, out_dev);
+    return cuda_check(cudaGetLastError(), "combine launch");
+}
+
+extern "C" int nnqs_energy_reduce(const double *eloc, const int64_t *counts, int64_t n,
+                                  double out[4], void *cuda_stream) {
+    if (n <= 0 || !eloc || !counts || !out)
+        return nnqs_set_error(NNQS_E_ARG, "nnqs_energy_reduce: bad arguments");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const int64_t chunks = (n + NNQS_REDUCE_CHUNK - 1) / NNQS_REDUCE_CHUNK;
+    double *buf = nullptr;
+    int rc = cuda_check(cudaMallocAsync((void **)&buf, sizeof(double) * (3 * chunks + 8), st), "alloc reduce");
+    if (rc) return rc;
+    double *part = buf, *o1 = buf + 3 * chunks, *o2 = o1 + 4;
+    k_chunk_partials<<<(unsigned)chunks, 256, 0, st>>>((const double2 *)eloc, counts, n, nullptr, part);
+    k_combine<<<1, 32, 0, st>>>(part, chunks, 1, o1);
+    k_chunk_partials<<<(unsigned)chunks, 256, 0, st>>>((const double2 *)eloc, counts, n, o1, part);
+    k_combine<<<1, 32, 0, st>>>(part, chunks, 2, o2);
+    double h[8];
+    rc = cuda_check(cudaMemcpyAsync(h, o1, sizeof(h), cudaMemcpyDeviceToHost, st), "read reduce");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync reduce");
+    cudaFreeAsync(buf, st);
+    if (rc) return rc;
+    out[0] = h[0]; out[1] = h[1]; out[2] = h[4]; out[3] = h[2];
+    if (!(h[2] > 0.0)) return nnqs_set_error(NNQS_E_EMPTY, "sum of counts is zero");
+    return NNQS_OK;
+}
+
+extern "C" int nnqs_local_energy_check(const double *eloc, int64_t n, void *cuda_stream) {
+    if (n < 0 || (n > 0 && !eloc)) return nnqs_set_error(NNQS_E_ARG, "nnqs_local_energy_check: bad arguments");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    int *flag = nullptr;
+    int rc = cuda_check(cudaMallocAsync((void **)&flag, sizeof(int), st), "alloc flag");
+    if (rc) return rc;
+    cudaMemsetAsync(flag, 0, sizeof(int), st);
+    if (n) k_any_nan<<<grid_for(2 * n, 256), 256, 0, st>>>(eloc, 2 * n, flag);
+    int h = 0;
+    rc = cuda_check(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "read flag");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
+    cudaFreeAsync(flag, st);
+    if (rc) return rc;
+    if (h) return nnqs_set_error(NNQS_E_ZERO_PSI, "some row has psi(x) = 0 (E_loc set to NaN)");
+    return NNQS_OK;
+}

@@ -1,0 +1,334 @@
+"""Parity of the CUDA path (through the C-ABI) with the CPU oracle.
+
+Tolerances (reading R14): per row |dE| <= 1e-10 * sum_x' |H_xx'| |psi(x')/psi(x)|
+(the oracle's scale output); bit-exact on flip masks, lookup indices and signs.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from oracle import dense, energy  # noqa: E402
+from oracle import rows as R  # noqa: E402
+from synth import configs as C  # noqa: E402
+from synth import samples as S  # noqa: E402
+
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def nnqs():
+    import __graft_entry__ as g
+    g.build()
+    from paper_2306_16705_b200 import nnqs as m
+    assert torch.cuda.is_available()
+    return m
+
+
+@pytest.fixture(scope="module")
+def dev():
+    return torch.device("cuda", 0)
+
+
+def _t(a, dev):
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint64:
+        a = a.view(np.int64)
+    return torch.from_numpy(a).to(dev)
+
+
+def _c(el):
+    el = el.cpu().numpy()
+    return el[:, 0] + 1j * el[:, 1]
+
+
+def _assert_close(got, ref, scale, what):
+    bad = ~(np.abs(got - ref) <= TOL * scale)
+    assert not bad.any(), f"{what}: {bad.sum()} rows off, worst {np.max(np.abs(got - ref) / scale)}"
+
+
+_HAMS = {}
+
+
+def ham_for(nnqs, c):
+    if c not in _HAMS:
+        m = C.molecule(c)
+        _HAMS[c] = nnqs.nnqs_ham_compress(m.h1, m.h2, m.n_qubits, m.e_core, device=0)
+    return _HAMS[c]
+
+
+# ------------------------------------------------------------------- compress
+@pytest.mark.parametrize("c", [1, 2, 3, 4])
+def test_device_ham_export_matches_host(nnqs, c):
+    m = C.molecule(c)
+    a = nnqs.nnqs_ham_compress(m.h1, m.h2, m.n_qubits, m.e_core, device=-1).export()
+    b = ham_for(nnqs, c).export()
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)
+    assert ham_for(nnqs, c).info()["device_bytes"] > 0
+
+
+# ----------------------------------------------------------------- exact mode
+@pytest.mark.parametrize("c", [1, 2])
+def test_exact_mode_random_psi(nnqs, dev, c):
+    """C1: all 16 configurations; C2: all 4096 (exact mode, random complex psi)."""
+    m = C.molecule(c)
+    lp = C.exact_random_psi(c)
+    ham = ham_for(nnqs, c)
+    tab = nnqs.nnqs_table_prepare(ham, 1, None, _t(lp, dev))
+    n = len(lp)
+    got = _c(nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n))
+    rows = np.stack([np.arange(n, dtype=np.uint64), np.zeros(n, dtype=np.uint64)], axis=1)
+    ref, scale = R.eloc(m.h1, m.h2, m.e_core, rows, lp, keys=None, logpsi=lp, with_scale=True)
+    _assert_close(got, ref, scale, f"C{c} exact")
+
+
+def test_exact_mode_fci_vector(nnqs, dev):
+    """C1 with the FCI vector (sector eigh): E_loc == E_0 on the 2 supported rows,
+    NaN (+ NNQS_E_ZERO_PSI) on the 14 rows with psi = 0 (reading R10, R17)."""
+    m = C.molecule(1)
+    keys = S.sector_keys(2, 1, 1)
+    e0, psi, _ = dense.ground_state(m.h1, m.h2, m.e_core, keys)
+    full = np.full((16, 2), [-np.inf, 0.0])
+    for k, a in zip(keys[:, 0], psi):
+        if abs(a) > 1e-12 * np.abs(psi).max():
+            full[int(k)] = [np.log(abs(a)), np.pi if a < 0 else 0.0]
+    ham = ham_for(nnqs, 1)
+    tab = nnqs.nnqs_table_prepare(ham, 1, None, _t(full, dev))
+    el = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=16)
+    got = _c(el)
+    sup = np.isfinite(full[:, 0])
+    assert sup.sum() == 2
+    assert np.all(np.abs(got[sup] - e0) <= TOL * abs(e0))
+    assert np.all(np.isnan(got[~sup].real))
+    with pytest.raises(nnqs.NNQSError) as e:
+        nnqs.nnqs_local_energy_check(el)
+    assert e.value.code == nnqs.NNQS_E_ZERO_PSI
+
+
+# --------------------------------------------------------- sample-aware mode
+def _sample_case(nnqs, dev, c, variant, row_idx=None):
+    m = C.molecule(c)
+    st = C.sample_table(c, variant)
+    ham = ham_for(nnqs, c)
+    tab = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(st.logpsi, dev))
+    if row_idx is None:
+        got = _c(nnqs.nnqs_local_energy(ham, tab, 0, n_rows=len(st.keys)))
+        rows, rlp = st.keys, st.logpsi
+    else:
+        rows, rlp = st.keys[row_idx], st.logpsi[row_idx]
+        got = _c(nnqs.nnqs_local_energy(ham, tab, rows=_t(rows, dev), row_logpsi=_t(rlp, dev)))
+    ref, scale = R.eloc(m.h1, m.h2, m.e_core, rows, rlp, keys=st.keys, logpsi=st.logpsi, with_scale=True)
+    return got, ref, scale
+
+
+@pytest.mark.parametrize("c,variant", [(2, "full"), (2, "half"), (3, "full"), (3, "half"), (4, "full")])
+def test_sample_mode_table_rows(nnqs, dev, c, variant):
+    """Every table entry as a row (the paper's ist/l slice)."""
+    got, ref, scale = _sample_case(nnqs, dev, c, variant)
+    _assert_close(got, ref, scale, f"C{c}/{variant}")
+
+
+@pytest.mark.parametrize("c", [2, 3, 4])
+def test_sample_mode_drawn_rows(nnqs, dev, c):
+    """Rows drawn with replacement (reading R19): C2 10^4, C3/C4 a seeded
+    10^4-row subset of the 10^5 draws (oracle cost), as explicit rows."""
+    st = C.sample_table(c, "full")
+    draws = C.row_draws(c, len(st.keys))[:10_000]
+    got, ref, scale = _sample_case(nnqs, dev, c, "full", draws)
+    _assert_close(got, ref, scale, f"C{c} drawn")
+
+
+def test_sample_mode_equals_exact_full_sector(nnqs, dev):
+    """Sample-aware with T = full sector == exact mode with psi = 0 off-sector."""
+    m = C.molecule(2)
+    st = C.sample_table(2, "full")
+    ham = ham_for(nnqs, 2)
+    full = np.full((4096, 2), [-np.inf, 0.0])
+    full[st.keys[:, 0].astype(np.int64)] = st.logpsi
+    ta = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(st.logpsi, dev))
+    tb = nnqs.nnqs_table_prepare(ham, 1, None, _t(full, dev))
+    a = _c(nnqs.nnqs_local_energy(ham, ta, 0, n_rows=len(st.keys)))
+    b = _c(nnqs.nnqs_local_energy(ham, tb, rows=_t(st.keys, dev), row_logpsi=_t(st.logpsi, dev)))
+    assert np.max(np.abs(a - b)) <= 1e-12 * np.max(np.abs(a))
+
+
+# ------------------------------------------------------------ C5: 120 qubits
+@pytest.fixture(scope="module")
+def c5(nnqs, dev):
+    m = C.molecule(5)
+    st = C.sample_table(5)
+    ham = ham_for(nnqs, 5)
+    tab = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(st.logpsi, dev))
+    return m, st, ham, tab
+
+
+def test_c5_sampled_rows(nnqs, dev, c5):
+    """120 spin orbitals, 10^6 unique near-HF samples: a seeded row subset plus
+    the HF row (most hits), evaluated as explicit rows."""
+    m, st, ham, tab = c5
+    idx = C.oracle_row_subset(5, len(st.keys), 16)
+    hf = np.argmax(st.counts)
+    idx = np.unique(np.concatenate([idx, [hf]]))
+    rows, rlp = st.keys[idx], st.logpsi[idx]
+    got = _c(nnqs.nnqs_local_energy(ham, tab, rows=_t(rows, dev), row_logpsi=_t(rlp, dev)))
+    ref, scale = R.eloc(m.h1, m.h2, m.e_core, rows, rlp, keys=st.keys, logpsi=st.logpsi, with_scale=True)
+    _assert_close(got, ref, scale, "C5 rows")
+
+
+# ---------------------------------------------- P3: coupled configurations
+@pytest.mark.parametrize("c,variant", [(2, "half"), (3, "full"), (4, "full")])
+def test_coupled_configurations_bit_exact(nnqs, dev, c, variant):
+    """Per row, the set of (x', table index) with |H_xx'| > tau equals the
+    oracle's, bit for bit; signs agree; GPU extras have |H| <= tau."""
+    m = C.molecule(c)
+    st = C.sample_table(c, variant)
+    ham = ham_for(nnqs, c)
+    tab = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(st.logpsi, dev))
+    sel = C.oracle_row_subset(c, len(st.keys), 24)
+    rid, gid, xp, tix, hv = nnqs.nnqs_coupled_debug(ham, tab, st.keys[sel])
+    tau = 1e-13 * max(np.abs(m.h1).max(), np.abs(m.h2).max())
+    x_all, _, _, _ = ham.export()
+    for j, i in enumerate(sel):
+        ridx, rh = R.row_hits(m.h1, m.h2, m.e_core, st.keys[i], keys=st.keys)
+        want = {int(a): b for a, b in zip(ridx, rh) if abs(b) > tau}
+        mine = rid == j
+        got = {int(a): b for a, b in zip(tix[mine], hv[mine])}
+        for k, g in zip(tix[mine], gid[mine]):      # x' = x ^ X_k and it is the table key
+            assert np.array_equal(st.keys[k], st.keys[i] ^ x_all[g])
+        assert set(k for k, v in got.items() if abs(v) > tau) == set(want)
+        for k, v in want.items():
+            assert np.sign(got[k]) == np.sign(v)
+            assert abs(got[k] - v) <= 1e-12 * max(1.0, abs(v))
+
+
+# ---------------------------------------------------- Pauli-level semantics
+def _pauli(nnqs, terms, nq):
+    X = [[x, 0] for x, _, _ in terms]
+    Z = [[z, 0] for _, z, _ in terms]
+    return nnqs.nnqs_ham_from_pauli(X, Z, [c for _, _, c in terms], nq, device=0)
+
+
+def test_spec_pauli_examples(nnqs, dev):
+    """SPEC.md:60-62, 253, 260 (Y = i X Z; <x'|P|x> with Z|b> = (-1)^b|b>)."""
+    c = 0.37
+    zero = np.zeros((1, 2))
+    # c Z0 on bit0 = 1 -> -c (T = {x})
+    h = _pauli(nnqs, [(0, 1, c)], 2)
+    k = np.array([[1, 0]], dtype=np.uint64)
+    t = nnqs.nnqs_table_prepare(h, 0, _t(k, dev), _t(zero, dev))
+    assert _c(nnqs.nnqs_local_energy(h, t, 0, n_rows=1))[0] == -c
+    # c Y0Y1 on |00> -> c * <11|Y0Y1|00> = -c ; uniform psi, exact mode
+    h = _pauli(nnqs, [(3, 3, c)], 2)
+    t = nnqs.nnqs_table_prepare(h, 1, None, _t(np.zeros((4, 2)), dev))
+    assert _c(nnqs.nnqs_local_energy(h, t, 0, n_rows=1))[0] == -c
+    # {c1 Z0, c2 Z1} on bit0 = 1, bit1 = 0 -> -c1 + c2
+    h = _pauli(nnqs, [(0, 1, 0.3), (0, 2, -0.45)], 2)
+    t = nnqs.nnqs_table_prepare(h, 0, _t(k, dev), _t(zero, dev))
+    assert _c(nnqs.nnqs_local_energy(h, t, 0, n_rows=1))[0] == -0.3 + -0.45
+    # T = {x}, c X0 -> 0 (absent x' contributes 0)
+    h = _pauli(nnqs, [(1, 0, c)], 2)
+    t = nnqs.nnqs_table_prepare(h, 0, _t(k, dev), _t(zero, dev))
+    assert _c(nnqs.nnqs_local_energy(h, t, 0, n_rows=1))[0] == 0.0
+    # c X0X1 with uniform psi -> c
+    h = _pauli(nnqs, [(3, 0, c)], 2)
+    t = nnqs.nnqs_table_prepare(h, 1, None, _t(np.zeros((4, 2)), dev))
+    assert np.all(_c(nnqs.nnqs_local_energy(h, t, 0, n_rows=4)) == c)
+
+
+# ------------------------------------------------------------------ reduce
+def test_reduce_matches_oracle(nnqs, dev):
+    rng = np.random.default_rng(5)
+    n = 70_001
+    e = rng.normal(-3.0, 0.4, size=n) + 1j * rng.normal(0, 0.01, size=n)
+    w = rng.integers(1, 100, size=n)
+    el = _t(np.stack([e.real, e.imag], axis=1), dev)
+    m, v, W = nnqs.nnqs_energy_reduce(el, _t(w.astype(np.int64), dev))
+    mr, vr, Wr = energy.energy(e, w)
+    assert W == Wr
+    assert abs(m - mr) <= TOL * np.sum(w * np.abs(e)) / Wr
+    assert abs(v - vr) <= TOL * vr + 2 * TOL * np.sqrt(vr) * np.abs(e).max()
+
+
+def test_reduce_spec_examples(nnqs, dev):
+    el = _t(np.array([[0.0, 0.0], [4.0, 0.0]]), dev)
+    m, v, W = nnqs.nnqs_energy_reduce(el, _t(np.array([3, 1], dtype=np.int64), dev))
+    assert (m, v, W) == (1.0, 3.0, 4.0)
+    with pytest.raises(nnqs.NNQSError) as e:
+        nnqs.nnqs_energy_reduce(el, _t(np.array([0, 0], dtype=np.int64), dev))
+    assert e.value.code == nnqs.NNQS_E_EMPTY
+
+
+# ---------------------------------------------- determinism and sharding
+def test_bitwise_determinism_and_slices(nnqs, dev):
+    """Same bits on a re-run, for explicit rows, and for any row slicing
+    (a row's summation order depends on the row alone)."""
+    st = C.sample_table(4, "full")
+    ham = ham_for(nnqs, 4)
+    tab = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(st.logpsi, dev))
+    n = len(st.keys)
+    a = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n).cpu().numpy()
+    b = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n).cpu().numpy()
+    c = nnqs.nnqs_local_energy(ham, tab, rows=_t(st.keys, dev), row_logpsi=_t(st.logpsi, dev)).cpu().numpy()
+    parts = [nnqs.nnqs_local_energy(ham, tab, s, n_rows=min(3001, n - s)).cpu().numpy() for s in range(0, n, 3001)]
+    d = np.concatenate(parts)
+    assert a.tobytes() == b.tobytes() == c.tobytes() == d.tobytes()
+
+
+def test_chunked_energy_is_partition_invariant(nnqs, dev):
+    """Chunk partials of chunk-aligned slices, combined in order, are bit-identical
+    to the single-call reduce (the multi-GPU energy path, Sec. 3.2 stage 4)."""
+    rng = np.random.default_rng(9)
+    n = 10 * 1024 + 77
+    e = np.stack([rng.normal(-2, 1, n), rng.normal(0, 0.1, n)], axis=1)
+    w = rng.integers(1, 9, size=n).astype(np.int64)
+    el, wc = _t(e, dev), _t(w, dev)
+    ref = nnqs.nnqs_energy_reduce(el, wc)
+    for P in (2, 3, 4):
+        bounds = np.linspace(0, n // 1024, P + 1).astype(int) * 1024
+        bounds[-1] = n
+        parts = [nnqs.nnqs_energy_chunk_partials(el[a:b], wc[a:b]) for a, b in zip(bounds[:-1], bounds[1:])]
+        allp = torch.cat(parts)
+        m1 = nnqs.nnqs_energy_combine(allp, 1)
+        parts2 = [nnqs.nnqs_energy_chunk_partials(el[a:b], wc[a:b], mean_dev=m1[:2].contiguous())
+                  for a, b in zip(bounds[:-1], bounds[1:])]
+        m2 = nnqs.nnqs_energy_combine(torch.cat(parts2), 2).cpu().numpy()
+        m1 = m1.cpu().numpy()
+        assert complex(m1[0], m1[1]) == ref[0] and m2[0] == ref[1] and m1[2] == ref[2]
+
+
+# ------------------------------------------------------------ edge cases
+def test_errors_and_edges(nnqs, dev):
+    ham = ham_for(nnqs, 2)
+    st = C.sample_table(2, "full")
+    bad = st.keys[::-1].copy()
+    with pytest.raises(nnqs.NNQSError) as e:
+        nnqs.nnqs_table_prepare(ham, 0, _t(bad, dev), _t(st.logpsi, dev))
+    assert e.value.code == nnqs.NNQS_E_TABLE
+    tab = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(st.logpsi, dev))
+    out = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=0)
+    assert out.shape[0] == 0
+    with pytest.raises(nnqs.NNQSError):
+        nnqs.nnqs_local_energy(ham, tab, len(st.keys) - 1, n_rows=2)
+    # a single-entry table and an empty table
+    one = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys[:1], dev), _t(st.logpsi[:1], dev))
+    got = _c(nnqs.nnqs_local_energy(ham, one, 0, n_rows=1))
+    m = C.molecule(2)
+    ref = R.eloc(m.h1, m.h2, m.e_core, st.keys[:1], st.logpsi[:1], keys=st.keys[:1], logpsi=st.logpsi[:1])
+    assert abs(got[0] - ref[0]) <= 1e-12 * abs(ref[0])
+
+
+def test_tiny_amplitude_row_fallback(nnqs, dev):
+    """A row with Re log psi(x) - s < -600 takes the per-term exp path (reading R11)."""
+    m = C.molecule(3)
+    st = C.sample_table(3, "full")
+    lp = st.logpsi.copy()
+    lp[5, 0] -= 620.0
+    lp[6, 0] += 30.0
+    ham = ham_for(nnqs, 3)
+    tab = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(lp, dev))
+    got = _c(nnqs.nnqs_local_energy(ham, tab, 0, n_rows=len(st.keys)))
+    ref, scale = R.eloc(m.h1, m.h2, m.e_core, st.keys, lp, keys=st.keys, logpsi=lp, with_scale=True)
+    _assert_close(got, ref, scale, "tiny psi")
