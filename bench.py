@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark of the local-energy hot path (BASELINE.json metric: local
+energies/s and coupled terms/s at 120 spin orbitals, 1/2/4/8 B200).
+
+One step = one pass of the whole path over one batch:
+  stage 2  all-gather of this rank's unique samples (keys | log psi), NCCL
+  A2       nnqs_table_prepare (order check, psi_hat, hash index)
+  A3-A6    nnqs_local_energy on this rank's chunk-aligned row slice
+  A7       count-weighted energy: chunk partials -> all-gather -> combine (x2)
+Workload C5 (BASELINE configs[4]): synthetic 120-spin-orbital molecule
+(2 irreps, 2,056,711 flip groups / 9,617,401 Pauli strings), 10^6 unique
+near-HF samples; rows = the 10^6 table entries, sharded over ranks (strong
+scaling: total work fixed).  A1 (compress) is once per molecule and timed
+separately ("can be neglected since it only needs to be done once").
+
+Usage: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "local energies/sec and coupled terms/sec at 120 spin orbitals, 1/2/4/8 B200"
+UNIT = "local energies/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5", choices=["C4", "C5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=0, help="oracle sample rows (0 = auto)")
+    return ap.parse_args()
+
+
+def workload(name):
+    from synth import configs as C
+    c = int(name[1])
+    mol = C.molecule(c)
+    st = C.sample_table(c, "full")
+    return c, mol, st
+
+
+def config_dict(name, mol, st, world, extra=None):
+    d = {"workload": f"{name}: {mol.name}, N={mol.n_qubits} spin orbitals, N_u={len(st.keys)} unique samples, "
+                     f"sample-aware mode, rows = all table entries sharded over ranks",
+         "n_spin_orbitals": mol.n_qubits, "n_unique": int(len(st.keys)), "n_rows": int(len(st.keys)),
+         "n_samples": int(st.counts.sum()), "parallelism": f"dp{world} (rows sharded, table replicated)",
+         "l2": "flushed between timed steps (256 MiB write outside the per-step events)"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p)), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def alu_peak_ops(sm_mhz):
+    """INT32 logic/add issue peak: 148 SMs x 4 SMSPs x 16 lanes/clk on the alu
+    pipe (LOP3/IADD3, rt_SMSP = 2; B300_MICROARCH.md 'Pipe rates') x SM clock."""
+    return 148 * 64 * sm_mhz * 1e6
+
+
+def cpu_baseline(mol, st, n_rows_req, seconds_target=15.0):
+    """The oracle (as it stands) on a bounded, seeded sample of this workload's
+    rows, on all host cores."""
+    import numpy as np
+    from oracle import rows as R
+    from synth import configs as C
+    idx = C.oracle_row_subset(5 if mol.n_qubits == 120 else 4, len(st.keys), 8)
+    t0 = time.perf_counter()
+    R.eloc(mol.h1, mol.h2, mol.e_core, st.keys[idx], st.logpsi[idx], keys=st.keys, logpsi=st.logpsi)
+    per_row = (time.perf_counter() - t0) / len(idx)
+    n = n_rows_req or int(max(16, min(4096, seconds_target / max(per_row, 1e-6))))
+    idx = C.oracle_row_subset(5 if mol.n_qubits == 120 else 4, len(st.keys), n)
+    t0 = time.perf_counter()
+    R.eloc(mol.h1, mol.h2, mol.e_core, st.keys[idx], st.logpsi[idx], keys=st.keys, logpsi=st.logpsi)
+    dt = time.perf_counter() - t0
+    return {"value": len(idx) / dt, "unit": UNIT, "cores": R.num_threads(), "kind": "oracle",
+            "sample": f"{len(idx)} seeded rows (seed 705) of the {len(st.keys)}-row table, full sample-aware "
+                      f"E_loc per row (plain term-by-term Eq. 9 + bisection), {dt:.1f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    name = args.config
+    c, mol, st = workload(name)
+    import numpy as np
+    from oracle import rows as R
+    from synth import configs as C
+    # each step: a bounded sample of the workload's rows through the oracle
+    n_per_step = 24 if c == 5 else 2000
+    times = []
+    for s in range(args.warmup + args.steps):
+        idx = np.sort(np.random.default_rng(900 + s).choice(len(st.keys), n_per_step, replace=False))
+        t0 = time.perf_counter()
+        R.eloc(mol.h1, mol.h2, mol.e_core, st.keys[idx], st.logpsi[idx], keys=st.keys, logpsi=st.logpsi)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = n_per_step * args.steps / tot
+    K = None
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": config_dict(name, mol, st, 1, {"reference_sample_rows_per_step": n_per_step}),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": R.num_threads(), "kind": "oracle",
+                            "sample": f"{n_per_step} seeded rows per step of the {len(st.keys)}-row table"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import __graft_entry__ as g
+    g.build()
+    from paper_2306_16705_b200 import distributed as D
+    from paper_2306_16705_b200 import nnqs
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    name = args.config
+    c, mol, st = workload(name)
+    n = len(st.keys)
+
+    t0 = time.perf_counter()
+    ham = nnqs.nnqs_ham_compress(mol.h1, mol.h2, mol.n_qubits, mol.e_core, device=local)
+    compress_s = time.perf_counter() - t0
+    info = ham.info()
+    K = info["n_groups"]
+
+    # this rank's shard of the unique samples (data-centric)
+    b, e = D.shard_bounds(n, world, rank)
+    keys_h = torch.from_numpy(st.keys.view(np.int64)[b:e].copy())
+    lp_h = torch.from_numpy(st.logpsi[b:e].copy())
+    cnt_h = torch.from_numpy(st.counts[b:e].copy())
+    keys_d, lp_d, cnt_d = keys_h.to(dev), lp_h.to(dev), cnt_h.to(dev)
+    n_local = e - b
+    stream = torch.cuda.current_stream()
+    eloc = torch.empty((n_local, 2), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev_k = []          # (start, end) events around nnqs_local_energy
+
+    def step(kd, ld, cd, timed):
+        if world > 1:
+            gk, gl = D.gather_samples(kd, ld)
+        else:
+            gk, gl = kd, ld
+        tab = nnqs.nnqs_table_prepare(ham, 0, gk, gl, stream=stream)
+        if timed:
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+        nnqs.nnqs_local_energy(ham, tab, b, n_rows=n_local, eloc_out=eloc, stream=stream)
+        if timed:
+            s1.record(stream)
+            ev_k.append((s0, s1))
+        if world > 1:
+            en = D.distributed_energy(eloc, cd, stream=stream)
+        else:
+            part = nnqs.nnqs_energy_chunk_partials(eloc, cd, stream=stream)
+            m1 = nnqs.nnqs_energy_combine(part, 1, stream=stream)
+            part2 = nnqs.nnqs_energy_chunk_partials(eloc, cd, mean_dev=m1[:2].contiguous(), stream=stream)
+            m2 = nnqs.nnqs_energy_combine(part2, 2, stream=stream)
+            en = torch.stack([m1[0], m1[1], m2[0], m1[2]])
+        return tab, en
+
+    for _ in range(args.warmup):
+        tab, en = step(keys_d, lp_d, cnt_d, False)
+        tab.close()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: K steps, per-step events, L2 flushed between
+    stats = torch.zeros(4, dtype=torch.int64, device=dev)
+    step_ms = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            tab, en = step(keys_d, lp_d, cnt_d, True)
+            a1.record(stream)
+            a1.synchronize()
+            step_ms.append(a0.elapsed_time(a1))
+            tab.close()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_total = sum(step_ms) / 1e3
+    kern_ms = [s.elapsed_time(t) for s, t in ev_k]
+    energy = en.cpu().numpy()
+    # stats of one launch (not timed)
+    tab = nnqs.nnqs_table_prepare(ham, 0, *(D.gather_samples(keys_d, lp_d) if world > 1 else (keys_d, lp_d)))
+    nnqs.nnqs_local_energy(ham, tab, b, n_rows=n_local, eloc_out=eloc, stats_out=stats)
+    st_local = stats.cpu().numpy().astype(np.int64)
+    tab.close()
+
+    # ---------------- e2e: host buffers through the C-ABI, copies inside the region
+    keys_p, lp_p, cnt_p = keys_h.pin_memory(), lp_h.pin_memory(), cnt_h.pin_memory()
+    res_p = torch.empty(4, dtype=torch.float64).pin_memory()
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        flush.fill_(1)
+        if world > 1:
+            dist.barrier()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        kd = keys_p.to(dev, non_blocking=True)
+        ld = lp_p.to(dev, non_blocking=True)
+        cd = cnt_p.to(dev, non_blocking=True)
+        tab, en = step(kd, ld, cd, False)
+        res_p.copy_(en, non_blocking=True)
+        a1.record(stream)
+        a1.synchronize()
+        if i >= args.warmup:
+            e2e_ms.append(a0.elapsed_time(a1))
+        tab.close()
+    h2d = keys_h.numel() * 8 + lp_h.numel() * 8 + cnt_h.numel() * 8
+    t_e2e = sum(e2e_ms) / 1e3
+
+    # ---------------- max over ranks
+    tt = torch.tensor([t_total, t_e2e, statistics.mean(kern_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        sts = torch.from_numpy(st_local).to(dev)
+        dist.all_reduce(sts)
+        st_local = sts.cpu().numpy()
+    t_total, t_e2e, kern_avg_ms = [float(v) for v in tt.cpu()]
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    value = n * args.steps / t_total
+    e2e_value = n * args.steps / t_e2e
+    pk, src = peaks()
+    clk_sum = clk.summary()
+    sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
+    alu_peak = alu_peak_ops(sm_mhz)
+    # algorithmic integer work of one local-energy launch (rank 0's slice):
+    # R_local * K' (row, group) pairs x 5 32-bit ops (128-bit XOR = 4 LOP3 +
+    # 1 membership decision) -- DESIGN.md 'Roofline'
+    r0 = D.shard_bounds(n, world, 0)
+    pairs_launch = (r0[1] - r0[0]) * K
+    achieved = pairs_launch * 5 / (kern_avg_ms / 1e3)
+    per_launch_traffic = None
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(name, mol, st, world, {
+            "n_groups": K, "n_terms": info["n_terms"], "ham_device_bytes": info["device_bytes"],
+            "compress_s": round(compress_s, 3)}),
+        "coupled_terms_per_s": n * K * args.steps / t_total,
+        "local_energy_kernel_ms": kern_avg_ms,
+        "kernel_share_of_step": kern_avg_ms / (1e3 * t_total / args.steps),
+        "energy": {"mean_re": float(energy[0]), "mean_im": float(energy[1]), "var": float(energy[2]),
+                   "W": float(energy[3])},
+        "stats": {"row_group_pairs": int(st_local[0]), "in_sector_pairs": int(st_local[1]),
+                  "hits": int(st_local[2]), "strings_evaluated": int(st_local[3])},
+        "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": alu_peak / 1e12,
+                     "unit": "Tops/s (INT32 ALU-pipe)", "frac": achieved / alu_peak, "traffic": per_launch_traffic,
+                     "peak_source": f"derived: 148 SMs x 64 INT32 lanes/clk (alu pipe) x {sm_mhz:.0f} MHz "
+                                    f"({src} sm_max_mhz)",
+                     "algorithmic_ops_per_launch": pairs_launch * 5},
+        "clocks": clk_sum,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 32},
+        "gpu_launches": 9 * args.steps,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        out["cpu_baseline"] = cpu_baseline(mol, st, args.cpu_rows)
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,90 @@
+"""Multi-GPU orchestration of the path with torch.distributed (NCCL on B200).
+
+The paper's data-centric scheme (Sec. 3.2): each process
+owns a batch of ~N_u/N_p unique samples; stage 2 all-gathers the samples
+(MPI_Allgather, N_u N_p (ceil(N/8)+16) bytes), stage 3 evaluates the local
+energies of the process's own batch against the replicated lookup table,
+stage 4 reduces the energy (MPI_Allreduce, 16 N_p bytes).
+
+Here: stage 2 is one NCCL all_gather_into_tensor of 32-byte records (key u64[2]
+| log-psi f64[2]); stage 4 all-gathers per-chunk energy partials (3 f64 per
+NNQS_REDUCE_CHUNK rows) and every rank combines them in global chunk order on
+the device, so the energy is bit-identical for any number of GPUs as long as
+row slices are chunk-aligned (shard_bounds).  This module only moves data;
+all arithmetic runs in libnnqs kernels.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+REDUCE_CHUNK = 1024
+
+
+def shard_bounds(n_rows: int, world: int, rank: int, chunk: int = REDUCE_CHUNK):
+    """Contiguous, chunk-aligned slice [begin, end) of n_rows for this rank
+    (the paper's ist / batch_size_cur_rank)."""
+    n_chunks = (n_rows + chunk - 1) // chunk
+    lo = (n_chunks * rank) // world
+    hi = (n_chunks * (rank + 1)) // world
+    return min(lo * chunk, n_rows), min(hi * chunk, n_rows)
+
+
+def all_gather_varlen(t: torch.Tensor, group=None) -> torch.Tensor:
+    """all_gather_into_tensor of per-rank tensors with different first
+    dimensions: gather the lengths, pad to the maximum, gather, strip."""
+    world = dist.get_world_size(group)
+    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
+    ns = torch.empty(world, dtype=torch.int64, device=t.device)
+    dist.all_gather_into_tensor(ns, n, group=group)
+    lens = [int(v) for v in ns.cpu()]
+    m = max(lens)
+    if t.shape[0] < m:
+        pad = torch.zeros((m - t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        t = torch.cat([t, pad])
+    out = torch.empty((world * m,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+    if all(v == m for v in lens):
+        return out
+    return torch.cat([out[r * m: r * m + lens[r]] for r in range(world)])
+
+
+def pack_records(keys: torch.Tensor, logpsi: torch.Tensor) -> torch.Tensor:
+    """[m,2] int64 keys + [m,2] float64 log-psi -> [m,4] int64 records (32 B/sample)."""
+    return torch.cat([keys.view(torch.int64), logpsi.view(torch.int64)], dim=1).contiguous()
+
+
+def unpack_records(rec: torch.Tensor):
+    keys = rec[:, :2].contiguous()
+    logpsi = rec[:, 2:].contiguous().view(torch.float64)
+    return keys, logpsi
+
+
+def gather_samples(local_keys: torch.Tensor, local_logpsi: torch.Tensor, group=None):
+    """Stage 2: every rank receives every unique sample.  Shards
+    are disjoint key ranges in rank order, so the concatenation stays sorted."""
+    rec = all_gather_varlen(pack_records(local_keys, local_logpsi), group)
+    return unpack_records(rec)
+
+
+def distributed_energy(eloc_local: torch.Tensor, counts_local: torch.Tensor, group=None, stream=None):
+    """Stage 4: count-weighted mean and variance (Eq. 6) over all
+    ranks' rows.  Returns a device f64[4] = (mean_re, mean_im, var, W)."""
+    from . import nnqs
+    p1 = nnqs.nnqs_energy_chunk_partials(eloc_local, counts_local, stream=stream)
+    allp = all_gather_varlen(p1[: _n_chunks(eloc_local)], group)
+    m1 = nnqs.nnqs_energy_combine(allp, 1, stream=stream)
+    p2 = nnqs.nnqs_energy_chunk_partials(eloc_local, counts_local, mean_dev=m1[:2].contiguous(), stream=stream)
+    allp2 = all_gather_varlen(p2[: _n_chunks(eloc_local)], group)
+    m2 = nnqs.nnqs_energy_combine(allp2, 2, stream=stream)
+    return torch.stack([m1[0], m1[1], m2[0], m1[2]])
+
+
+def _n_chunks(t: torch.Tensor) -> int:
+    return (t.shape[0] + REDUCE_CHUNK - 1) // REDUCE_CHUNK
+
+
+def comm_bytes_paper(n_u: int, n_qubits: int, n_p: int, n_params: int) -> int:
+    """The paper's per-iteration communication volume:
+    N_u N_p (ceil(N/8) + 16) + 16 N_p + 8 M N_p bytes."""
+    return n_u * n_p * (-(-n_qubits // 8) + 16) + 16 * n_p + 8 * n_params * n_p
