@@ -144,6 +144,20 @@ int nnqs_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_
                       const double *row_logpsi, int64_t n_rows, double *eloc_out,
                       int64_t *stats_out, void *cuda_stream);
 
+/*
+ * Algorithm selection (process-wide):
+ *   0 (default) -- rows == NULL in sample-aware mode with a Hamiltonian from
+ *       nnqs_ham_compress: the alpha/beta-factorised enumeration (DESIGN.md
+ *       "structured path"): the same (row, group) pairs with x' in the table
+ *       as the literal loop, found by scanning the table's alpha-/beta-string
+ *       lists; stats_out[1] then counts list entries / probes examined.
+ *       Every other call uses the literal loop.
+ *   1 -- always the literal loop of Algorithm 2 (every row x every group,
+ *       sector test, hash lookup of x').
+ */
+int nnqs_set_algorithm(int algorithm);
+int nnqs_get_algorithm(void);
+
 /* Synchronises cuda_stream; NNQS_E_ZERO_PSI if any of eloc (device f64[n][2]) is NaN. */
 int nnqs_local_energy_check(const double *eloc, int64_t n, void *cuda_stream);
 

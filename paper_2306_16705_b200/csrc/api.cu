@@ -66,8 +66,11 @@ int check_symmetry(const double *h1, const double *h2, int n) {
     return NNQS_OK;
 }
 
+int g_algorithm = 0;
+
 int finish_ham(nnqs_ham h, int device, nnqs_ham *out) {
     h->device = device;
+    nnqs_spin_index_build(h->host, h->spin);
     h->n_groups = (int64_t)h->host.off.size() - 1;
     h->n_terms = (int64_t)h->host.d.size();
     if (device < 0) {          // host-only handle: export / info only
@@ -78,6 +81,7 @@ int finish_ham(nnqs_ham h, int device, nnqs_ham *out) {
     if (!g.ok) return nnqs_set_error(NNQS_E_CUDA, "cudaSetDevice failed");
     configure_pool(device);
     int rc = nnqs_ham_upload(h);
+    if (!rc) rc = nnqs_spin_index_upload(h);
     if (rc) {
         nnqs_ham_release(h);
         delete h;
@@ -87,6 +91,8 @@ int finish_ham(nnqs_ham h, int device, nnqs_ham *out) {
     return NNQS_OK;
 }
 }  // namespace
+
+int nnqs_algorithm() { return g_algorithm; }
 
 int nnqs_set_error(int code, const std::string &msg) {
     g_last_error = msg;
@@ -181,6 +187,7 @@ int nnqs_ham_free(nnqs_ham h) {
     if (h->device >= 0) {
         DeviceGuard g(h->device);
         nnqs_ham_release(h);
+        nnqs_spin_index_release(h);
     }
     delete h;
     return NNQS_OK;
@@ -212,6 +219,7 @@ int nnqs_table_prepare(nnqs_ham h, int mode, const uint64_t *keys, const double 
     }
     configure_pool(h->device);
     int rc = nnqs_table_build(t, keys, logpsi, cuda_stream);
+    if (!rc && mode == 0) rc = nnqs_table_build_spin(h, t, cuda_stream);
     if (rc) {
         nnqs_table_release(t);
         delete t;
@@ -225,6 +233,7 @@ int nnqs_table_free(nnqs_table t) {
     if (!t) return NNQS_OK;
     {
         DeviceGuard g(t->device);
+        nnqs_table_release_spin(t);
         nnqs_table_release(t);
     }
     delete t;
@@ -263,8 +272,20 @@ int nnqs_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_
     }
     DeviceGuard g(h->device);
     if (!g.ok) return nnqs_set_error(NNQS_E_CUDA, "cudaSetDevice failed");
+    if (!rows && t->spin_ready && h->spin.ok && g_algorithm != 1) {
+        if (n_rows == 0) return NNQS_OK;
+        return nnqs_launch_local_energy_spin(h, t, row_begin, n_rows, eloc_out, stats_out, cuda_stream);
+    }
     return nnqs_launch_local_energy(h, t, row_begin, rows, row_logpsi, n_rows, eloc_out, stats_out, cuda_stream);
 }
+
+int nnqs_set_algorithm(int algorithm) {
+    if (algorithm != 0 && algorithm != 1) return nnqs_set_error(NNQS_E_ARG, "algorithm must be 0 or 1");
+    g_algorithm = algorithm;
+    return NNQS_OK;
+}
+
+int nnqs_get_algorithm(void) { return g_algorithm; }
 
 int nnqs_coupled_debug(nnqs_ham h, nnqs_table t, const uint64_t *rows_host, int64_t n_rows,
                        int64_t max_pairs, int64_t *row_id, int64_t *group_id, uint64_t *xprime,

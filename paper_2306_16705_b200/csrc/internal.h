@@ -41,6 +41,24 @@ int nnqs_compress_host(const double *h1, const double *h2, int n, double e_core,
 int nnqs_from_pauli_host(const u64 *xm, const u64 *zm, const double *cre, const double *cim,
                          int64_t n_terms, int n_qubits, double tol, HostTable &out);
 
+// alpha/beta-factorised index of a spin-conserving table (structured.cu):
+// every flip group is X = 0, an alpha pair, a beta pair, an alpha quad, a
+// beta quad, or alpha pair x beta pair (the single / double excitations of
+// Eq. (9)); group ids are reachable from the orbital indices without a search.
+struct SpinIndex {
+    bool ok = false;
+    int n = 0;                        // spatial orbitals (<= 64)
+    int64_t P = 0, Q = 0;             // n(n-1)/2, C(n,4)
+    int32_t diag_k = -1;
+    std::vector<int32_t> pair_k[2];   // [P]   2-site groups per spin
+    std::vector<int32_t> quad_k[2];   // [Q]   4-site same-spin groups
+    std::vector<int32_t> ab_k;        // [P*P] alpha pair x beta pair groups
+};
+int nnqs_spin_index_build(const HostTable &H, SpinIndex &S);
+struct nnqs_ham_s;
+int nnqs_spin_index_upload(struct nnqs_ham_s *h);
+void nnqs_spin_index_release(struct nnqs_ham_s *h);
+
 struct DeviceHam {
     // group arrays [K]
     void *gx = nullptr;       // ulonglong2 X mask
@@ -50,11 +68,16 @@ struct DeviceHam {
     // term arrays [Nh]
     void *tz = nullptr;       // ulonglong2 Z mask
     double *td = nullptr;     // fused coefficient d
+    // spin index (structured path)
+    int32_t *pair_k[2] = {nullptr, nullptr};
+    int32_t *quad_k[2] = {nullptr, nullptr};
+    int32_t *ab_k = nullptr;
     int64_t bytes = 0;
 };
 
 struct nnqs_ham_s {
     HostTable host;
+    SpinIndex spin;
     DeviceHam dev;
     int device = 0;
     int64_t n_groups = 0, n_terms = 0;
@@ -73,7 +96,26 @@ struct nnqs_table_s {
     u64 *shift_key = nullptr; // device: order-preserving key of s = max Re logpsi
     int *flag = nullptr;      // device: order violation flag
     int64_t bytes = 0;
+    // alpha/beta string index (structured path, mode 0)
+    bool spin_ready = false;
+    void *spin_buf = nullptr; // one allocation holding the arrays below
+    u64 *sa = nullptr, *sb = nullptr;          // [n] alpha / beta occupation strings
+    int32_t *ga_of = nullptr, *gb_of = nullptr;// [n] alpha-group / beta-group of entry i
+    int32_t *offA = nullptr, *offB = nullptr;  // [n+1] CSR over alpha / beta groups
+    u64 *listA_b = nullptr;                    // [n] entries sorted by (a, b): beta string
+    int32_t *listA_idx = nullptr;              //     ... and table index
+    u64 *listB_a = nullptr;                    // [n] entries sorted by (b, a): alpha string
+    int32_t *listB_idx = nullptr;
+    u64 *ah_keys = nullptr;                    // alpha string -> alpha group (open addressing)
+    int32_t *ah_vals = nullptr;
+    u64 ah_mask = 0;
 };
+
+int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream);
+void nnqs_table_release_spin(nnqs_table t);
+int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, int64_t n_rows,
+                                  double *eloc, int64_t *stats, void *stream);
+int nnqs_algorithm();
 
 // device side (kernels.cu)
 int nnqs_ham_upload(nnqs_ham h);

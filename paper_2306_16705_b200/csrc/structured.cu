@@ -1,0 +1,608 @@
+// structured.cu -- the alpha/beta-factorised ("string-driven") local-energy
+// path: same sum as Algorithm 2, same set of
+// (row, group) pairs with x' = x ^ X_k in the sample table,
+// enumerated from the table side instead of the group side.
+//
+// A row x = (a, b) (alpha / beta occupation strings) couples through a group
+// of the compressed table (Fig. 6(c)) only to
+//   (i)   x' = (a'', b): a'' in A(b) = {alpha strings paired with b in T},
+//         X = alpha pair (2-site group) or alpha quad (4-site same-spin);
+//   (ii)  x' = (a, b''): b'' in B(a), X = beta pair or beta quad;
+//   (iii) x' = (a ^ u, b ^ v): u an alpha single (one occupied, one empty),
+//         v a beta single, X = u x v (4-site opposite-spin);
+// plus the diagonal group (X = 0, x' = x).  Scanning the table-side lists
+// A(b), B(a) and B(a ^ u) visits every x' of the table that some group can
+// reach, so the hit set equals the literal loop's (tests: P3 parity), while
+// the work per row drops from K' (2.06e6 groups at 120 qubits) to the list
+// lengths.  H_xx' itself is still the group's Pauli sum
+// sum_i d_i (-1)^{popc(x & Z_i)} (reading R1).
+//
+// Accumulation order of a row depends on the row and the table only (fixed
+// lane assignment, fixed butterfly reduction): bit-identical for any row
+// slicing / number of GPUs.
+#include <cuda_runtime.h>
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "internal.h"
+
+__constant__ u64 c_hs[128];   // same GF(2) hash columns as kernels.cu (per translation unit)
+
+namespace {
+
+bool g_hs_ready[64] = {false};
+
+int ensure_hs(int device) {
+    if (device < 0 || device >= 64) return NNQS_E_ARG;
+    if (g_hs_ready[device]) return NNQS_OK;
+    u64 cols[128];
+    nnqs_hash_columns(cols);
+    cudaError_t e = cudaMemcpyToSymbol(c_hs, cols, sizeof(cols));
+    if (e != cudaSuccess) return nnqs_set_error(NNQS_E_CUDA, cudaGetErrorString(e));
+    g_hs_ready[device] = true;
+    return NNQS_OK;
+}
+
+inline int cuda_check(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return NNQS_OK;
+    return nnqs_set_error(e == cudaErrorMemoryAllocation ? NNQS_E_NOMEM : NNQS_E_CUDA,
+                          std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+inline int grid_for(int64_t n, int block) {
+    int64_t g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > 148 * 32) g = 148 * 32;
+    return (int)g;
+}
+
+__host__ __device__ __forceinline__ int64_t pair_rank(int p, int q, int n) {   // p < q
+    return (int64_t)p * (2 * n - p - 1) / 2 + (q - p - 1);
+}
+
+__host__ __device__ __forceinline__ int64_t quad_rank(int p1, int p2, int p3, int p4) {  // colex, p1<p2<p3<p4
+    return (int64_t)p1 + (int64_t)p2 * (p2 - 1) / 2 + (int64_t)p3 * (p3 - 1) * (p3 - 2) / 6 +
+           (int64_t)p4 * (p4 - 1) * (p4 - 2) * (p4 - 3) / 24;
+}
+
+__host__ __device__ __forceinline__ u64 mix64(u64 z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// ------------------------------------------------------------- device views
+struct SpinView {
+    int n;
+    int64_t P;
+    const int32_t *pair_k0, *pair_k1, *quad_k0, *quad_k1, *ab_k;
+    int32_t diag_k;
+};
+
+struct GroupView {
+    const uint32_t *goff;
+    const ulonglong2 *tz;
+    const double *td;
+};
+
+struct TabSpin {
+    int64_t n;
+    const ulonglong2 *keys;
+    const double2 *logpsi;
+    const double2 *psi_hat;
+    const u64 *slots;
+    u64 bucket_mask;
+    const u64 *shift_key;
+    const u64 *sa, *sb;
+    const int32_t *ga_of, *gb_of, *offA, *offB;
+    const u64 *listA_b, *listB_a;
+    const int32_t *listA_idx, *listB_idx;
+    const u64 *ah_keys;
+    const int32_t *ah_vals;
+    u64 ah_mask;
+};
+
+__device__ __forceinline__ double dkey_inv2(u64 k) {
+    if (k == 0) return 0.0;
+    u64 b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFULL) : ~k;
+    return __longlong_as_double((long long)b);
+}
+
+__device__ __forceinline__ double flip_sign2(double d, int parity) {
+    return __longlong_as_double(__double_as_longlong(d) ^ ((long long)parity << 63));
+}
+
+// H_{x', x} = sum_{i in group k} d_i (-1)^{popc(x & Z_i)}  (one lane)
+__device__ __forceinline__ double group_value1(const GroupView &G, int32_t k, u64 x0, u64 x1,
+                                               unsigned long long &n_str) {
+    const uint32_t b = __ldg(G.goff + k), e = __ldg(G.goff + k + 1);
+    double hv = 0.0;
+    for (uint32_t i = b; i < e; ++i) {
+        const ulonglong2 Z = __ldg(G.tz + i);
+        hv += flip_sign2(__ldg(G.td + i), (__popcll(x0 & Z.x) + __popcll(x1 & Z.y)) & 1);
+    }
+    n_str += e - b;
+    return hv;
+}
+
+// spread the bits of a (alpha, spin 0) / b (beta, spin 1) onto qubits 2p+s
+__device__ __forceinline__ void spread_bit(int p, int s, u64 &w0, u64 &w1) {
+    const int j = 2 * p + s;
+    if (j < 64) w0 ^= 1ULL << j;
+    else w1 ^= 1ULL << (j - 64);
+}
+
+__device__ __forceinline__ int32_t alpha_lookup(const TabSpin &T, u64 a) {
+    u64 s = mix64(a) & T.ah_mask;
+    while (true) {
+        const int32_t v = __ldg(T.ah_vals + s);
+        if (v < 0) return -1;
+        if (__ldg(T.ah_keys + s) == a) return v;
+        s = (s + 1) & T.ah_mask;
+    }
+}
+
+__device__ __forceinline__ int64_t probe_key(const TabSpin &T, u64 h, u64 p0, u64 p1) {
+    u64 b = h & T.bucket_mask;
+    const uint32_t fp = (uint32_t)(h >> 32);
+    while (true) {
+        const ulonglong2 *bk = reinterpret_cast<const ulonglong2 *>(T.slots + 4 * b);
+        const ulonglong2 s01 = __ldg(bk), s23 = __ldg(bk + 1);
+        const u64 s[4] = {s01.x, s01.y, s23.x, s23.y};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (s[i] == 0xFFFFFFFFFFFFFFFFULL) return -1;
+            if ((uint32_t)(s[i] >> 32) == fp) {
+                const uint32_t r = (uint32_t)s[i];
+                const ulonglong2 k = __ldg(T.keys + r);
+                if (k.x == p0 && k.y == p1) return (int64_t)r;
+            }
+        }
+        b = (b + 1) & T.bucket_mask;
+    }
+}
+
+// index of the o-th set bit (0-based) of a 64-bit word
+__device__ __forceinline__ int nth_set(u64 w, int o) {
+    const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
+    const int c = __popc(lo);
+    if (o < c) return (int)__fns(lo, 0, o + 1);
+    return 32 + (int)__fns(hi, 0, o - c + 1);
+}
+
+// group id of the same-spin excitation d (2 or 4 bits, within one spin string)
+__device__ __forceinline__ int32_t same_spin_group(const SpinView &S, int spin, u64 d, int c) {
+    const int p1 = __ffsll((long long)d) - 1;
+    d &= d - 1;
+    const int p2 = __ffsll((long long)d) - 1;
+    if (c == 2) return __ldg((spin ? S.pair_k1 : S.pair_k0) + pair_rank(p1, p2, S.n));
+    d &= d - 1;
+    const int p3 = __ffsll((long long)d) - 1;
+    d &= d - 1;
+    const int p4 = __ffsll((long long)d) - 1;
+    return __ldg((spin ? S.quad_k1 : S.quad_k0) + quad_rank(p1, p2, p3, p4));
+}
+
+#define SCAN_LIMIT 8192
+
+// one warp per row; rows are table entries [row_begin, row_begin + n_rows)
+__global__ void __launch_bounds__(256) k_eloc_spin(SpinView S, GroupView G, TabSpin T, int64_t row_begin,
+                                                   int64_t n_rows, double2 *out,
+                                                   unsigned long long *stats, unsigned long long pairs) {
+    if (stats && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(stats, pairs);
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const double s = dkey_inv2(*T.shift_key);
+    const u64 nmask = S.n >= 64 ? ~0ULL : ((1ULL << S.n) - 1);
+    unsigned long long c_cand = 0, c_hit = 0, c_str = 0;
+    for (int64_t r = warp; r < n_rows; r += nwarps) {
+        const int64_t i = row_begin + r;
+        const ulonglong2 xk = T.keys[i];
+        const u64 x0 = xk.x, x1 = xk.y;
+        const double2 lx = T.logpsi[i];
+        if (!(lx.x > -INFINITY)) {
+            if (lane == 0) out[r] = make_double2(NAN, NAN);
+            continue;
+        }
+        const double rel = lx.x - s;
+        const bool direct = rel < -600.0;
+        const u64 a = T.sa[i], b = T.sb[i];
+        double ar = 0.0, ai = 0.0;
+        // contribution of one hit: H * psi(x')/psi(x) (scaled by psi_hat(x))
+        auto add = [&](double hv, int64_t idx) {
+            double2 ps;
+            if (!direct) {
+                ps = __ldg(T.psi_hat + idx);
+            } else {
+                const double2 l = T.logpsi[idx];
+                const double m = exp(l.x - lx.x);
+                double sn, cs;
+                sincos(l.y - lx.y, &sn, &cs);
+                ps = make_double2(m * cs, m * sn);
+            }
+            ar = fma(hv, ps.x, ar);
+            ai = fma(hv, ps.y, ai);
+        };
+        // ---- diagonal group: warp-cooperative Pauli sum, fixed reduction
+        if (S.diag_k >= 0) {
+            const uint32_t gb = __ldg(G.goff + S.diag_k), ge = __ldg(G.goff + S.diag_k + 1);
+            double hv = 0.0;
+            for (uint32_t t = gb + lane; t < ge; t += 32) {
+                const ulonglong2 Z = __ldg(G.tz + t);
+                hv += flip_sign2(__ldg(G.td + t), (__popcll(x0 & Z.x) + __popcll(x1 & Z.y)) & 1);
+            }
+            for (int o = 16; o; o >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, o);
+            if (lane == 0) {
+                add(hv, i);
+                c_str += ge - gb;
+                ++c_hit;
+            }
+        }
+        // ---- (i) same beta string: x' = (a'', b), a'' in A(b)
+        {
+            const int32_t g = T.gb_of[i];
+            const int32_t jb = T.offB[g], je = T.offB[g + 1];
+            for (int32_t j = jb + lane; j < je; j += 32) {
+                const u64 d = a ^ __ldg(T.listB_a + j);
+                const int c = __popcll(d);
+                ++c_cand;
+                if ((c != 2 && c != 4) || 2 * __popcll(a & d) != c) continue;
+                const int32_t k = same_spin_group(S, 0, d, c);
+                if (k < 0) continue;
+                ++c_hit;
+                add(group_value1(G, k, x0, x1, c_str), __ldg(T.listB_idx + j));
+            }
+        }
+        // ---- (ii) same alpha string: x' = (a, b''), b'' in B(a)
+        const int32_t ga = T.ga_of[i];
+        {
+            const int32_t jb = T.offA[ga], je = T.offA[ga + 1];
+            for (int32_t j = jb + lane; j < je; j += 32) {
+                const u64 d = b ^ __ldg(T.listA_b + j);
+                const int c = __popcll(d);
+                ++c_cand;
+                if ((c != 2 && c != 4) || 2 * __popcll(b & d) != c) continue;
+                const int32_t k = same_spin_group(S, 1, d, c);
+                if (k < 0) continue;
+                ++c_hit;
+                add(group_value1(G, k, x0, x1, c_str), __ldg(T.listA_idx + j));
+            }
+        }
+        // ---- (iii) alpha single u x beta single v
+        {
+            const u64 va = ~a & nmask, vb = ~b & nmask;
+            const int noa = __popcll(a), nva = __popcll(va);
+            const int nob = __popcll(b), nvb = __popcll(vb);
+            const int combos = noa * nva;
+            const int bsingles = nob * nvb;
+            u64 hxx = 0;                       // GF(2) hash of the full key x (probe mode)
+            for (u64 w = x0; w; w &= w - 1) hxx ^= c_hs[__ffsll((long long)w) - 1];
+            for (u64 w = x1; w; w &= w - 1) hxx ^= c_hs[64 + __ffsll((long long)w) - 1];
+            // lanes test 32 alpha singles at a time; the adjacent ones present in
+            // the table are then processed one by one by the whole warp
+            for (int c0 = 0; c0 < combos; c0 += 32) {
+                const int cidx = c0 + lane;
+                int p = 0, q = 0;
+                int32_t g2 = -1;
+                if (cidx < combos) {
+                    p = nth_set(a, cidx / nva);
+                    q = nth_set(va, cidx % nva);
+                    g2 = alpha_lookup(T, a ^ (1ULL << p) ^ (1ULL << q));
+                    ++c_cand;
+                }
+                unsigned ball = __ballot_sync(0xffffffffu, g2 >= 0);
+                while (ball) {
+                    const int src = __ffs(ball) - 1;
+                    ball &= ball - 1;
+                    const int pp = __shfl_sync(0xffffffffu, p, src);
+                    const int qq = __shfl_sync(0xffffffffu, q, src);
+                    const int32_t gg = __shfl_sync(0xffffffffu, g2, src);
+                    const int32_t *abk = S.ab_k + pair_rank(min(pp, qq), max(pp, qq), S.n) * S.P;
+                    const int32_t jb = T.offA[gg], je = T.offA[gg + 1];
+                    if (je - jb <= SCAN_LIMIT) {
+                        for (int32_t j = jb + lane; j < je; j += 32) {
+                            const u64 d = b ^ __ldg(T.listA_b + j);
+                            ++c_cand;
+                            if (__popcll(d) != 2 || __popcll(b & d) != 1) continue;
+                            const int r1 = __ffsll((long long)d) - 1;
+                            const int r2 = 63 - __clzll((long long)d);
+                            const int32_t k = __ldg(abk + pair_rank(r1, r2, S.n));
+                            if (k < 0) continue;
+                            ++c_hit;
+                            add(group_value1(G, k, x0, x1, c_str), __ldg(T.listA_idx + j));
+                        }
+                    } else {
+                        // long list: probe each beta single of b in the full-key hash
+                        u64 u0 = 0, u1 = 0;
+                        spread_bit(pp, 0, u0, u1);
+                        spread_bit(qq, 0, u0, u1);
+                        const u64 hu = hxx ^ c_hs[2 * pp] ^ c_hs[2 * qq];
+                        for (int cb = lane; cb < bsingles; cb += 32) {
+                            const int r1 = nth_set(b, cb / nvb), r2 = nth_set(vb, cb % nvb);
+                            const int32_t k = __ldg(abk + pair_rank(min(r1, r2), max(r1, r2), S.n));
+                            ++c_cand;
+                            if (k < 0) continue;
+                            u64 w0 = u0, w1 = u1;
+                            spread_bit(r1, 1, w0, w1);
+                            spread_bit(r2, 1, w0, w1);
+                            const int64_t idx = probe_key(T, hu ^ c_hs[2 * r1 + 1] ^ c_hs[2 * r2 + 1], x0 ^ w0, x1 ^ w1);
+                            if (idx < 0) continue;
+                            ++c_hit;
+                            add(group_value1(G, k, x0, x1, c_str), idx);
+                        }
+                    }
+                }
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            ar += __shfl_xor_sync(0xffffffffu, ar, o);
+            ai += __shfl_xor_sync(0xffffffffu, ai, o);
+        }
+        if (lane == 0) {
+            double2 e;
+            if (direct) {
+                e = make_double2(ar, ai);
+            } else {
+                const double m = exp(-rel);
+                double sn, cs;
+                sincos(-lx.y, &sn, &cs);
+                const double ir = m * cs, ii = m * sn;
+                e = make_double2(ar * ir - ai * ii, ar * ii + ai * ir);
+            }
+            out[r] = e;
+        }
+    }
+    if (stats) {
+        for (int o = 16; o; o >>= 1) {
+            c_cand += __shfl_xor_sync(0xffffffffu, c_cand, o);
+            c_hit += __shfl_xor_sync(0xffffffffu, c_hit, o);
+            c_str += __shfl_xor_sync(0xffffffffu, c_str, o);
+        }
+        if (lane == 0) {
+            atomicAdd((unsigned long long *)stats + 1, c_cand);
+            atomicAdd((unsigned long long *)stats + 2, c_hit);
+            atomicAdd((unsigned long long *)stats + 3, c_str);
+        }
+    }
+}
+
+// ------------------------------------------------------ table-side index build
+__device__ __forceinline__ u64 gather_spin(u64 w, int s) {     // bits s, s+2, ... of w -> 32 bits
+    w = (w >> s) & 0x5555555555555555ULL;
+    w = (w | (w >> 1)) & 0x3333333333333333ULL;
+    w = (w | (w >> 2)) & 0x0F0F0F0F0F0F0F0FULL;
+    w = (w | (w >> 4)) & 0x00FF00FF00FF00FFULL;
+    w = (w | (w >> 8)) & 0x0000FFFF0000FFFFULL;
+    w = (w | (w >> 16)) & 0x00000000FFFFFFFFULL;
+    return w;
+}
+
+__global__ void k_split(const ulonglong2 *keys, int64_t n, u64 *sa, u64 *sb, int32_t *iota) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const ulonglong2 k = keys[i];
+        sa[i] = gather_spin(k.x, 0) | (gather_spin(k.y, 0) << 32);
+        sb[i] = gather_spin(k.x, 1) | (gather_spin(k.y, 1) << 32);
+        iota[i] = (int32_t)i;
+    }
+}
+
+__global__ void k_gather64(const u64 *src, const int32_t *perm, int64_t n, u64 *dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[perm[i]];
+}
+
+__global__ void k_heads(const u64 *ksorted, int64_t n, int32_t *flag) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x)
+        flag[j] = (j == 0 || ksorted[j] != ksorted[j - 1]) ? 1 : 0;
+}
+
+// gid = inclusive scan of heads - 1; lists + CSR + group-of-entry
+__global__ void k_csr(const u64 *ksorted, const int32_t *perm, const int32_t *incl, int64_t n,
+                      const u64 *other, int32_t *off, int32_t *g_of, u64 *list_other, int32_t *list_idx,
+                      u64 *hkeys, int32_t *hvals, u64 hmask) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t g = incl[j] - 1;
+        const int32_t e = perm[j];
+        g_of[e] = g;
+        list_other[j] = other[e];
+        list_idx[j] = e;
+        const bool head = (j == 0 || ksorted[j] != ksorted[j - 1]);
+        if (head) {
+            off[g] = (int32_t)j;
+            if (hkeys) {
+                const u64 key = ksorted[j];
+                u64 s = mix64(key) & hmask;
+                while (atomicCAS((int *)(hvals + s), -1, g) != -1) s = (s + 1) & hmask;
+                hkeys[s] = key;
+            }
+        }
+        if (j == n - 1) off[g + 1] = (int32_t)n;
+    }
+}
+
+}  // namespace
+
+// ============================================================== host side
+int nnqs_spin_index_build(const HostTable &H, SpinIndex &S) {
+    S = SpinIndex();
+    const int N = H.n_qubits;
+    if (!H.conserving || N > 128 || (N & 1)) return NNQS_OK;
+    const int n = N / 2;
+    S.n = n;
+    S.P = (int64_t)n * (n - 1) / 2;
+    S.Q = n >= 4 ? (int64_t)n * (n - 1) * (n - 2) * (n - 3) / 24 : 0;
+    for (int s = 0; s < 2; ++s) {
+        S.pair_k[s].assign(std::max<int64_t>(S.P, 1), -1);
+        S.quad_k[s].assign(std::max<int64_t>(S.Q, 1), -1);
+    }
+    S.ab_k.assign(std::max<int64_t>(S.P * S.P, 1), -1);
+    const int64_t K = (int64_t)H.off.size() - 1;
+    for (int64_t k = 0; k < K; ++k) {
+        int pos[2][4], cnt[2] = {0, 0};
+        bool bad = false;
+        for (int w = 0; w < 2 && !bad; ++w) {
+            u64 x = H.x[2 * k + w];
+            while (x) {
+                const int j = 64 * w + __builtin_ctzll(x);
+                x &= x - 1;
+                const int s = j & 1, p = j >> 1;
+                if (cnt[s] == 4) { bad = true; break; }
+                pos[s][cnt[s]++] = p;        // ascending (qubits ascend)
+            }
+        }
+        if (bad) return NNQS_OK;
+        const int ca = cnt[0], cb = cnt[1];
+        if (ca == 0 && cb == 0) S.diag_k = (int32_t)k;
+        else if (ca == 2 && cb == 0) S.pair_k[0][pair_rank(pos[0][0], pos[0][1], n)] = (int32_t)k;
+        else if (ca == 0 && cb == 2) S.pair_k[1][pair_rank(pos[1][0], pos[1][1], n)] = (int32_t)k;
+        else if (ca == 4 && cb == 0) S.quad_k[0][quad_rank(pos[0][0], pos[0][1], pos[0][2], pos[0][3])] = (int32_t)k;
+        else if (ca == 0 && cb == 4) S.quad_k[1][quad_rank(pos[1][0], pos[1][1], pos[1][2], pos[1][3])] = (int32_t)k;
+        else if (ca == 2 && cb == 2)
+            S.ab_k[pair_rank(pos[0][0], pos[0][1], n) * S.P + pair_rank(pos[1][0], pos[1][1], n)] = (int32_t)k;
+        else return NNQS_OK;               // not a single/double excitation pattern
+    }
+    S.ok = true;
+    return NNQS_OK;
+}
+
+int nnqs_spin_index_upload(nnqs_ham h) {
+    SpinIndex &S = h->spin;
+    DeviceHam &D = h->dev;
+    if (!S.ok) return NNQS_OK;
+    int rc;
+    for (int s = 0; s < 2; ++s) {
+        size_t bp = 4 * S.pair_k[s].size(), bq = 4 * S.quad_k[s].size();
+        if ((rc = cuda_check(cudaMalloc((void **)&D.pair_k[s], bp), "alloc pair_k"))) return rc;
+        if ((rc = cuda_check(cudaMalloc((void **)&D.quad_k[s], bq), "alloc quad_k"))) return rc;
+        if ((rc = cuda_check(cudaMemcpy(D.pair_k[s], S.pair_k[s].data(), bp, cudaMemcpyHostToDevice), "copy pair_k"))) return rc;
+        if ((rc = cuda_check(cudaMemcpy(D.quad_k[s], S.quad_k[s].data(), bq, cudaMemcpyHostToDevice), "copy quad_k"))) return rc;
+        D.bytes += (int64_t)(bp + bq);
+    }
+    size_t bab = 4 * S.ab_k.size();
+    if ((rc = cuda_check(cudaMalloc((void **)&D.ab_k, bab), "alloc ab_k"))) return rc;
+    if ((rc = cuda_check(cudaMemcpy(D.ab_k, S.ab_k.data(), bab, cudaMemcpyHostToDevice), "copy ab_k"))) return rc;
+    D.bytes += (int64_t)bab;
+    return NNQS_OK;
+}
+
+void nnqs_spin_index_release(nnqs_ham h) {
+    DeviceHam &D = h->dev;
+    for (int s = 0; s < 2; ++s) {
+        cudaFree(D.pair_k[s]);
+        cudaFree(D.quad_k[s]);
+        D.pair_k[s] = D.quad_k[s] = nullptr;
+    }
+    cudaFree(D.ab_k);
+    D.ab_k = nullptr;
+}
+
+int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
+    if (!h->spin.ok || t->mode != 0 || t->n == 0) return NNQS_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = t->n;
+    if (n >= (1LL << 31) - 2) return NNQS_OK;
+    u64 hs = 1;
+    while (hs < 2 * (u64)n) hs <<= 1;
+    // temp storage for the two sorts
+    size_t tmp_sort = 0, tmp_scan = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, (const u64 *)nullptr, (u64 *)nullptr,
+                                    (const int32_t *)nullptr, (int32_t *)nullptr, (int)n, 0, 64, st);
+    cub::DeviceScan::InclusiveSum(nullptr, tmp_scan, (const int32_t *)nullptr, (int32_t *)nullptr, (int)n, st);
+    const size_t tmp = std::max(tmp_sort, tmp_scan);
+    // persistent arrays
+    auto r16 = [](size_t b) { return (b + 15) & ~size_t(15); };
+    const size_t pers = 2 * r16(8 * n) + 2 * r16(4 * n) + 2 * r16(4 * (n + 1)) + 2 * r16(8 * n) + 2 * r16(4 * n) +
+                        r16(8 * hs) + r16(4 * hs) + 16;
+    // scratch: iota, perm1, perm2 (int32), k1, k2 (u64), flags, incl (int32), cub temp
+    const size_t scr = 5 * r16(4 * n) + 2 * r16(8 * n) + r16(tmp) + 16;
+    char *buf = nullptr;
+    int rc = cuda_check(cudaMallocAsync((void **)&buf, pers, st), "alloc spin index");
+    if (rc) return rc;
+    char *scratch = nullptr;
+    rc = cuda_check(cudaMallocAsync((void **)&scratch, scr, st), "alloc spin scratch");
+    if (rc) { cudaFreeAsync(buf, st); return rc; }
+    t->spin_buf = buf;
+    auto take = [&](size_t bytes) { char *p = buf; buf += (bytes + 15) & ~size_t(15); return p; };
+    t->sa = (u64 *)take(8 * n);
+    t->sb = (u64 *)take(8 * n);
+    t->ga_of = (int32_t *)take(4 * n);
+    t->gb_of = (int32_t *)take(4 * n);
+    t->offA = (int32_t *)take(4 * (n + 1));
+    t->offB = (int32_t *)take(4 * (n + 1));
+    t->listA_b = (u64 *)take(8 * n);
+    t->listA_idx = (int32_t *)take(4 * n);
+    t->listB_a = (u64 *)take(8 * n);
+    t->listB_idx = (int32_t *)take(4 * n);
+    t->ah_keys = (u64 *)take(8 * hs);
+    t->ah_vals = (int32_t *)take(4 * hs);
+    t->ah_mask = hs - 1;
+    t->bytes += (int64_t)pers;
+    char *sp = scratch;
+    auto stake = [&](size_t bytes) { char *p = sp; sp += (bytes + 15) & ~size_t(15); return p; };
+    int32_t *iota = (int32_t *)stake(4 * n), *perm1 = (int32_t *)stake(4 * n), *perm2 = (int32_t *)stake(4 * n);
+    u64 *k1 = (u64 *)stake(8 * n), *k2 = (u64 *)stake(8 * n);
+    int32_t *flags = (int32_t *)stake(4 * n), *incl = (int32_t *)stake(4 * n);
+    void *ctmp = stake(tmp);
+    const int g = grid_for(n, 256);
+    k_split<<<g, 256, 0, st>>>((const ulonglong2 *)t->keys, n, t->sa, t->sb, iota);
+    cudaMemsetAsync(t->ah_vals, 0xFF, 4 * hs, st);
+    for (int pass = 0; pass < 2; ++pass) {
+        // pass 0: sort by (a, b) -> alpha groups, lists of b;  pass 1: by (b, a)
+        const u64 *primary = pass == 0 ? t->sa : t->sb;
+        const u64 *secondary = pass == 0 ? t->sb : t->sa;
+        size_t tb = tmp;
+        cub::DeviceRadixSort::SortPairs(ctmp, tb, secondary, k1, iota, perm1, (int)n, 0, 64, st);
+        k_gather64<<<g, 256, 0, st>>>(primary, perm1, n, k2);
+        tb = tmp;
+        cub::DeviceRadixSort::SortPairs(ctmp, tb, k2, k1, perm1, perm2, (int)n, 0, 64, st);
+        k_heads<<<g, 256, 0, st>>>(k1, n, flags);
+        tb = tmp;
+        cub::DeviceScan::InclusiveSum(ctmp, tb, flags, incl, (int)n, st);
+        if (pass == 0)
+            k_csr<<<g, 256, 0, st>>>(k1, perm2, incl, n, t->sb, t->offA, t->ga_of, t->listA_b, t->listA_idx,
+                                     t->ah_keys, t->ah_vals, t->ah_mask);
+        else
+            k_csr<<<g, 256, 0, st>>>(k1, perm2, incl, n, t->sa, t->offB, t->gb_of, t->listB_a, t->listB_idx,
+                                     nullptr, nullptr, 0);
+    }
+    cudaFreeAsync(scratch, st);
+    rc = cuda_check(cudaGetLastError(), "spin index kernels");
+    if (rc) return rc;
+    t->spin_ready = true;
+    return NNQS_OK;
+}
+
+void nnqs_table_release_spin(nnqs_table t) {
+    if (t->spin_buf) cudaFreeAsync(t->spin_buf, (cudaStream_t)t->stream);
+    t->spin_buf = nullptr;
+    t->spin_ready = false;
+}
+
+int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, int64_t n_rows, double *eloc,
+                                  int64_t *stats, void *stream) {
+    const SpinIndex &S = h->spin;
+    const DeviceHam &D = h->dev;
+    SpinView sv{S.n, S.P, D.pair_k[0], D.pair_k[1], D.quad_k[0], D.quad_k[1], D.ab_k, S.diag_k};
+    GroupView gv{D.goff, (const ulonglong2 *)D.tz, D.td};
+    TabSpin tv{t->n, (const ulonglong2 *)t->keys, (const double2 *)t->logpsi, (const double2 *)t->psi_hat,
+               t->slots, t->bucket_mask, t->shift_key, t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB,
+               t->listA_b, t->listB_a, t->listA_idx, t->listB_idx, t->ah_keys, t->ah_vals, t->ah_mask};
+    const int64_t threads = n_rows * 32;
+    int g = (int)std::min<int64_t>((threads + 255) / 256, 148 * 64);
+    if (g < 1) g = 1;
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = ensure_hs(h->device);
+    if (rc) return rc;
+    // stats[0] = row-group pairs resolved (the literal loop's R * K')
+    const unsigned long long pairs = (unsigned long long)n_rows * (unsigned long long)h->n_groups;
+    k_eloc_spin<<<g, 256, 0, st>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc, (unsigned long long *)stats,
+                                   pairs);
+    return cuda_check(cudaGetLastError(), "structured local energy launch");
+}

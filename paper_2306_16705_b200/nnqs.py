@@ -35,6 +35,8 @@ _sig = {
     "nnqs_table_info": ([P, P, P, P], ctypes.c_int),
     "nnqs_local_energy": ([P, P, I64, P, P, I64, P, P, P], ctypes.c_int),
     "nnqs_local_energy_check": ([P, I64, P], ctypes.c_int),
+    "nnqs_set_algorithm": ([ctypes.c_int], ctypes.c_int),
+    "nnqs_get_algorithm": ([], ctypes.c_int),
     "nnqs_energy_chunk_partials": ([P, P, I64, P, P, P], ctypes.c_int),
     "nnqs_energy_combine": ([P, I64, ctypes.c_int, P, P], ctypes.c_int),
     "nnqs_energy_reduce": ([P, P, I64, P, P], ctypes.c_int),
@@ -203,6 +205,18 @@ def nnqs_local_energy(ham: Hamiltonian, table: Table, row_begin: int = 0, rows=N
     _check(_lib.nnqs_local_energy(ham.handle, table.handle, int(row_begin), _dev_ptr(rows), _dev_ptr(row_logpsi),
                                   int(n_rows), _dev_ptr(eloc_out), _dev_ptr(stats_out), _stream(stream)))
     return eloc_out
+
+
+ALGO_AUTO, ALGO_LITERAL = 0, 1
+
+
+def nnqs_set_algorithm(algorithm: int):
+    """0 = auto (alpha/beta-factorised enumeration for table rows), 1 = literal loop."""
+    _check(_lib.nnqs_set_algorithm(int(algorithm)))
+
+
+def nnqs_get_algorithm() -> int:
+    return int(_lib.nnqs_get_algorithm())
 
 
 def nnqs_local_energy_check(eloc, stream=None):

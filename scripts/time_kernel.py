@@ -9,11 +9,13 @@ from synth import configs as C
 
 c = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 nrows = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+algo = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 dev = torch.device("cuda", 0)
 m = C.molecule(c); st = C.sample_table(c)
 t = time.time(); ham = nnqs.nnqs_ham_compress(m.h1, m.h2, m.n_qubits, m.e_core, device=0); print("compress", time.time() - t, ham.info())
 keys = torch.from_numpy(st.keys.view(np.int64)).to(dev); lp = torch.from_numpy(st.logpsi).to(dev)
 tab = nnqs.nnqs_table_prepare(ham, 0, keys, lp)
+nnqs.nnqs_set_algorithm(algo)
 n = nrows or len(st.keys)
 out = torch.empty((n, 2), dtype=torch.float64, device=dev)
 stats = torch.zeros(4, dtype=torch.int64, device=dev)
@@ -23,5 +25,5 @@ for it in range(3):
     e0.record(); nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, eloc_out=out, stats_out=stats); e1.record(); e1.synchronize()
     ms = e0.elapsed_time(e1)
     s = stats.cpu().numpy()
-    print(f"C{c} rows={n} K={ham.info()['n_groups']} {ms:.3f} ms  rows/s={n/ms*1e3:.3e} pairs/s={n*ham.info()['n_groups']/ms*1e3:.3e} stats={s} hits/row={s[2]/n:.1f}")
+    print(f"algo={algo} C{c} rows={n} K={ham.info()['n_groups']} {ms:.3f} ms  rows/s={n/ms*1e3:.3e} pairs/s={n*ham.info()['n_groups']/ms*1e3:.3e} stats={s} hits/row={s[2]/n:.1f}")
 e0.record(); tab2 = nnqs.nnqs_table_prepare(ham, 0, keys, lp); e1.record(); e1.synchronize(); print("table_prepare ms", e0.elapsed_time(e1))

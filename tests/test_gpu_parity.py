@@ -178,6 +178,40 @@ def test_c5_sampled_rows(nnqs, dev, c5):
     _assert_close(got, ref, scale, "C5 rows")
 
 
+def test_c5_full_launch_sampled(nnqs, dev, c5):
+    """The bench launch: every one of the 10^6 table rows in one call; sampled
+    rows (seeded subset + HF row) checked against the oracle one by one."""
+    m, st, ham, tab = c5
+    n = len(st.keys)
+    stats = torch.zeros(4, dtype=torch.int64, device=dev)
+    el = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, stats_out=stats)
+    nnqs.nnqs_local_energy_check(el)
+    idx = np.unique(np.concatenate([C.oracle_row_subset(5, n, 12), [np.argmax(st.counts)]]))
+    got = _c(el)[idx]
+    ref, scale = R.eloc(m.h1, m.h2, m.e_core, st.keys[idx], st.logpsi[idx], keys=st.keys, logpsi=st.logpsi,
+                        with_scale=True)
+    _assert_close(got, ref, scale, "C5 full launch")
+    s = stats.cpu().numpy()
+    assert s[0] == n * ham.info()["n_groups"] and s[2] > n
+
+
+def test_c5_structured_equals_literal_hits(nnqs, dev, c5):
+    """On a 4096-row slice of C5: identical hit and string counts for the two
+    enumerations, and E_loc within tolerance of each other."""
+    m, st, ham, tab = c5
+    s1 = torch.zeros(4, dtype=torch.int64, device=dev)
+    s2 = torch.zeros(4, dtype=torch.int64, device=dev)
+    a = _c(nnqs.nnqs_local_energy(ham, tab, 500_000, n_rows=4096, stats_out=s1))
+    nnqs.nnqs_set_algorithm(nnqs.ALGO_LITERAL)
+    try:
+        b = _c(nnqs.nnqs_local_energy(ham, tab, 500_000, n_rows=4096, stats_out=s2))
+    finally:
+        nnqs.nnqs_set_algorithm(nnqs.ALGO_AUTO)
+    s1, s2 = s1.cpu().numpy(), s2.cpu().numpy()
+    assert s1[2] == s2[2] and s1[3] == s2[3]
+    assert np.max(np.abs(a - b) / np.maximum(np.abs(b), 1.0)) < 1e-9
+
+
 # ---------------------------------------------- P3: coupled configurations
 @pytest.mark.parametrize("c,variant", [(2, "half"), (3, "full"), (4, "full")])
 def test_coupled_configurations_bit_exact(nnqs, dev, c, variant):
@@ -263,18 +297,48 @@ def test_reduce_spec_examples(nnqs, dev):
 
 # ---------------------------------------------- determinism and sharding
 def test_bitwise_determinism_and_slices(nnqs, dev):
-    """Same bits on a re-run, for explicit rows, and for any row slicing
-    (a row's summation order depends on the row alone)."""
+    """Same bits on a re-run and for any row slicing (a row's summation order
+    depends on the row alone) -- structured path (table rows) and literal
+    path (explicit rows) separately."""
     st = C.sample_table(4, "full")
     ham = ham_for(nnqs, 4)
     tab = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(st.logpsi, dev))
     n = len(st.keys)
     a = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n).cpu().numpy()
     b = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n).cpu().numpy()
-    c = nnqs.nnqs_local_energy(ham, tab, rows=_t(st.keys, dev), row_logpsi=_t(st.logpsi, dev)).cpu().numpy()
     parts = [nnqs.nnqs_local_energy(ham, tab, s, n_rows=min(3001, n - s)).cpu().numpy() for s in range(0, n, 3001)]
     d = np.concatenate(parts)
-    assert a.tobytes() == b.tobytes() == c.tobytes() == d.tobytes()
+    assert a.tobytes() == b.tobytes() == d.tobytes()
+    c1 = nnqs.nnqs_local_energy(ham, tab, rows=_t(st.keys, dev), row_logpsi=_t(st.logpsi, dev)).cpu().numpy()
+    c2 = nnqs.nnqs_local_energy(ham, tab, rows=_t(st.keys[::-1].copy(), dev),
+                                row_logpsi=_t(st.logpsi[::-1].copy(), dev)).cpu().numpy()[::-1]
+    assert c1.tobytes() == np.ascontiguousarray(c2).tobytes()
+
+
+@pytest.mark.parametrize("c,variant", [(2, "half"), (3, "full"), (4, "full")])
+def test_structured_equals_literal(nnqs, dev, c, variant):
+    """The alpha/beta-factorised enumeration finds exactly the literal loop's
+    hits (equal hit counts) and the same E_loc (within the parity tolerance)."""
+    m = C.molecule(c)
+    st = C.sample_table(c, variant)
+    ham = ham_for(nnqs, c)
+    tab = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(st.logpsi, dev))
+    n = len(st.keys)
+    s1 = torch.zeros(4, dtype=torch.int64, device=dev)
+    s2 = torch.zeros(4, dtype=torch.int64, device=dev)
+    a = _c(nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, stats_out=s1))
+    nnqs.nnqs_set_algorithm(nnqs.ALGO_LITERAL)
+    try:
+        b = _c(nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, stats_out=s2))
+    finally:
+        nnqs.nnqs_set_algorithm(nnqs.ALGO_AUTO)
+    s1, s2 = s1.cpu().numpy(), s2.cpu().numpy()
+    assert s1[0] == s2[0] == n * ham.info()["n_groups"]
+    assert s1[2] == s2[2]                       # identical hit sets (counts)
+    assert s1[3] == s2[3]                       # identical Pauli strings evaluated
+    ref, scale = R.eloc(m.h1, m.h2, m.e_core, st.keys, st.logpsi, keys=st.keys, logpsi=st.logpsi, with_scale=True)
+    _assert_close(a, ref, scale, "structured")
+    _assert_close(b, ref, scale, "literal")
 
 
 def test_chunked_energy_is_partition_invariant(nnqs, dev):
