@@ -109,6 +109,14 @@ struct nnqs_table_s {
     u64 *ah_keys = nullptr;                    // alpha string -> alpha group (open addressing)
     int32_t *ah_vals = nullptr;
     u64 ah_mask = 0;
+    // deletion-key multimap for heavy string groups (see structured.cu)
+    void *mm = nullptr;                        // unique-key hash slots {u64 key, u32 meta, u32 run}
+    u64 mm_mask = 0;
+    int32_t *mm_run = nullptr;                 // [n_runs+1] run starts into mm_val
+    int32_t *mm_val = nullptr;                 // entry indices sorted by (meta, key, entry)
+    u64 *mm_str = nullptr;                     // ... and the entry's varying string
+    void *mm_buf = nullptr;
+    int32_t thr_single = 0, thr_double = 0;    // list-length thresholds
 };
 
 int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream);

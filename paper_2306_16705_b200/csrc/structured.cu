@@ -102,7 +102,26 @@ struct TabSpin {
     const u64 *ah_keys;
     const int32_t *ah_vals;
     u64 ah_mask;
+    const ulonglong2 *mm;     // deletion multimap: unique (key, meta) -> run id (y = meta | run << 32)
+    u64 mm_mask;
+    const int32_t *mm_run, *mm_val;
+    const u64 *mm_str;
+    int32_t thr_single, thr_double;
 };
+
+// ---------------------------------------------------------------- multimap
+// Deletion keys: two occupation strings of one spin differ by a single
+// excitation iff they share a 1-deletion (the string minus one occupied
+// orbital), by a double iff they share a 2-deletion.  For heavy groups the
+// table entries are indexed by (tag, group id, deletion) so that a row finds
+// its coupled x' with 15 (singles) or 105 (doubles) probes instead of a scan.
+//   tag 0: (alpha group, beta string minus 1 orbital)   tag 1: minus 2
+//   tag 2: (beta group, alpha string minus 1 orbital)   tag 3: minus 2
+#define MM_EMPTY 0xFFFFFFFFu
+__host__ __device__ __forceinline__ uint32_t mm_meta(int tag, int32_t g) { return ((uint32_t)tag << 30) | (uint32_t)g; }
+__host__ __device__ __forceinline__ u64 mm_hash(u64 key, uint32_t meta) {
+    return mix64(key ^ ((u64)meta * 0x9E3779B97F4A7C15ULL));
+}
 
 __device__ __forceinline__ double dkey_inv2(u64 k) {
     if (k == 0) return 0.0;
@@ -119,6 +138,7 @@ __device__ __forceinline__ double group_value1(const GroupView &G, int32_t k, u6
                                                unsigned long long &n_str) {
     const uint32_t b = __ldg(G.goff + k), e = __ldg(G.goff + k + 1);
     double hv = 0.0;
+#pragma unroll 4
     for (uint32_t i = b; i < e; ++i) {
         const ulonglong2 Z = __ldg(G.tz + i);
         hv += flip_sign2(__ldg(G.td + i), (__popcll(x0 & Z.x) + __popcll(x1 & Z.y)) & 1);
@@ -185,14 +205,52 @@ __device__ __forceinline__ int32_t same_spin_group(const SpinView &S, int spin, 
     return __ldg((spin ? S.quad_k1 : S.quad_k0) + quad_rank(p1, p2, p3, p4));
 }
 
-#define SCAN_LIMIT 8192
+// multimap lookup: [beg, end) into mm_val of the entries stored under (key, meta)
+__device__ __forceinline__ void mm_find(const TabSpin &T, u64 key, uint32_t meta, int32_t &beg, int32_t &end) {
+    u64 pos = mm_hash(key, meta) & T.mm_mask;
+    beg = end = 0;
+    while (true) {
+        const ulonglong2 v = __ldg(T.mm + pos);
+        const uint32_t run = (uint32_t)(v.y >> 32);
+        if (run == MM_EMPTY) return;
+        if (v.x == key && (uint32_t)v.y == meta) {
+            beg = __ldg(T.mm_run + run);
+            end = __ldg(T.mm_run + run + 1);
+            return;
+        }
+        pos = (pos + 1) & T.mm_mask;
+    }
+}
 
-// one warp per row; rows are table entries [row_begin, row_begin + n_rows)
-__global__ void __launch_bounds__(256) k_eloc_spin(SpinView S, GroupView G, TabSpin T, int64_t row_begin,
+// (i, j) = the c-th index pair i < j in colex order (c = j(j-1)/2 + i)
+__device__ __forceinline__ void nth_pair(int c, int &i, int &j) {
+    j = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)c)) * 0.5f);
+    while (j * (j - 1) / 2 > c) --j;
+    while ((j + 1) * j / 2 <= c) ++j;
+    i = c - j * (j - 1) / 2;
+}
+
+#define SCAN_LIMIT 8192
+#define WARPS_PER_BLOCK 8
+#define QCAP 64
+
+// one warp per row; rows are table entries [row_begin, row_begin + n_rows).
+// Candidate x' are found by warp-uniform, 4-way unrolled scans of the table's
+// string lists; hits (group k, table index) go to a per-warp queue and are
+// evaluated 32 at a time, one per lane (slot s -> lane s mod 32, so the
+// summation order of a row is fixed by the row and the table).
+__global__ void __launch_bounds__(256, 2) k_eloc_spin(SpinView S, GroupView G, TabSpin T, int64_t row_begin,
                                                    int64_t n_rows, double2 *out,
-                                                   unsigned long long *stats, unsigned long long pairs) {
+                                                   unsigned long long *stats, unsigned long long pairs,
+                                                   int phase_mask) {
+    __shared__ int2 s_q[WARPS_PER_BLOCK][QCAP];
+    __shared__ uint8_t s_orb[WARPS_PER_BLOCK][4][64];   // occ(a), vir(a), occ(b), vir(b) of the row
     if (stats && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(stats, pairs);
     const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    int2 *q = s_q[threadIdx.x >> 5];
+    uint8_t *occA = s_orb[threadIdx.x >> 5][0], *virA = s_orb[threadIdx.x >> 5][1];
+    uint8_t *occB = s_orb[threadIdx.x >> 5][2], *virB = s_orb[threadIdx.x >> 5][3];
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const double s = dkey_inv2(*T.shift_key);
@@ -211,7 +269,16 @@ __global__ void __launch_bounds__(256) k_eloc_spin(SpinView S, GroupView G, TabS
         const bool direct = rel < -600.0;
         const u64 a = T.sa[i], b = T.sb[i];
         double ar = 0.0, ai = 0.0;
-        // contribution of one hit: H * psi(x')/psi(x) (scaled by psi_hat(x))
+        __syncwarp();
+        for (int j = lane; j < S.n; j += 32) {       // orbital lists (replace nth-set-bit searches)
+            const u64 below = (1ULL << j) - 1;
+            if ((a >> j) & 1) occA[__popcll(a & below)] = (uint8_t)j;
+            else virA[j - __popcll(a & below)] = (uint8_t)j;
+            if ((b >> j) & 1) occB[__popcll(b & below)] = (uint8_t)j;
+            else virB[j - __popcll(b & below)] = (uint8_t)j;
+        }
+        __syncwarp();
+        // contribution of one hit: H * psi(x') (psi_hat scale; divided by psi_hat(x) at the end)
         auto add = [&](double hv, int64_t idx) {
             double2 ps;
             if (!direct) {
@@ -226,10 +293,51 @@ __global__ void __launch_bounds__(256) k_eloc_spin(SpinView S, GroupView G, TabS
             ar = fma(hv, ps.x, ar);
             ai = fma(hv, ps.y, ai);
         };
+        int qn = 0;                                  // warp-uniform queue length
+        auto flush = [&](int cnt) {                  // lanes < cnt evaluate q[lane]
+            __syncwarp();
+            int2 e = make_int2(-1, 0);
+            uint32_t gb0 = 0, ge0 = 0;
+            if (lane < cnt) {
+                e = q[lane];
+                gb0 = __ldg(G.goff + e.x);
+                ge0 = __ldg(G.goff + e.x + 1);
+                ++c_hit;
+            }
+            const bool big = lane < cnt && ge0 - gb0 > 32;
+            if (lane < cnt && !big) add(group_value1(G, e.x, x0, x1, c_str), e.y);
+            unsigned bigs = __ballot_sync(0xffffffffu, big);
+            while (bigs) {                               // long groups: whole warp, fixed reduction
+                const int src = __ffs(bigs) - 1;
+                bigs &= bigs - 1;
+                const uint32_t b1 = __shfl_sync(0xffffffffu, gb0, src), e1 = __shfl_sync(0xffffffffu, ge0, src);
+                double hv = 0.0;
+                for (uint32_t t = b1 + lane; t < e1; t += 32) {
+                    const ulonglong2 Z = __ldg(G.tz + t);
+                    hv += flip_sign2(__ldg(G.td + t), (__popcll(x0 & Z.x) + __popcll(x1 & Z.y)) & 1);
+                }
+                for (int o = 16; o; o >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, o);
+                if (lane == src) {
+                    add(hv, e.y);
+                    c_str += e1 - b1;
+                }
+            }
+            __syncwarp();
+            if (lane < qn - cnt) q[lane] = q[lane + cnt];
+            __syncwarp();
+            qn -= cnt;
+        };
+        auto push = [&](int32_t k, int32_t idx) {    // all lanes; k < 0 = no hit
+            const unsigned m = __ballot_sync(0xffffffffu, k >= 0);
+            if (k >= 0) q[qn + __popc(m & lt_mask)] = make_int2(k, idx);
+            qn += __popc(m);
+            if (qn >= 32) flush(32);
+        };
         // ---- diagonal group: warp-cooperative Pauli sum, fixed reduction
-        if (S.diag_k >= 0) {
+        if (S.diag_k >= 0 && (phase_mask & 1)) {
             const uint32_t gb = __ldg(G.goff + S.diag_k), ge = __ldg(G.goff + S.diag_k + 1);
             double hv = 0.0;
+#pragma unroll 4
             for (uint32_t t = gb + lane; t < ge; t += 32) {
                 const ulonglong2 Z = __ldg(G.tz + t);
                 hv += flip_sign2(__ldg(G.td + t), (__popcll(x0 & Z.x) + __popcll(x1 & Z.y)) & 1);
@@ -241,102 +349,199 @@ __global__ void __launch_bounds__(256) k_eloc_spin(SpinView S, GroupView G, TabS
                 ++c_hit;
             }
         }
-        // ---- (i) same beta string: x' = (a'', b), a'' in A(b)
-        {
-            const int32_t g = T.gb_of[i];
-            const int32_t jb = T.offB[g], je = T.offB[g + 1];
-            for (int32_t j = jb + lane; j < je; j += 32) {
-                const u64 d = a ^ __ldg(T.listB_a + j);
-                const int c = __popcll(d);
-                ++c_cand;
-                if ((c != 2 && c != 4) || 2 * __popcll(a & d) != c) continue;
-                const int32_t k = same_spin_group(S, 0, d, c);
-                if (k < 0) continue;
-                ++c_hit;
-                add(group_value1(G, k, x0, x1, c_str), __ldg(T.listB_idx + j));
-            }
-        }
-        // ---- (ii) same alpha string: x' = (a, b''), b'' in B(a)
-        const int32_t ga = T.ga_of[i];
-        {
-            const int32_t jb = T.offA[ga], je = T.offA[ga + 1];
-            for (int32_t j = jb + lane; j < je; j += 32) {
-                const u64 d = b ^ __ldg(T.listA_b + j);
-                const int c = __popcll(d);
-                ++c_cand;
-                if ((c != 2 && c != 4) || 2 * __popcll(b & d) != c) continue;
-                const int32_t k = same_spin_group(S, 1, d, c);
-                if (k < 0) continue;
-                ++c_hit;
-                add(group_value1(G, k, x0, x1, c_str), __ldg(T.listA_idx + j));
-            }
-        }
-        // ---- (iii) alpha single u x beta single v
-        {
-            const u64 va = ~a & nmask, vb = ~b & nmask;
-            const int noa = __popcll(a), nva = __popcll(va);
-            const int nob = __popcll(b), nvb = __popcll(vb);
-            const int combos = noa * nva;
-            const int bsingles = nob * nvb;
-            u64 hxx = 0;                       // GF(2) hash of the full key x (probe mode)
-            for (u64 w = x0; w; w &= w - 1) hxx ^= c_hs[__ffsll((long long)w) - 1];
-            for (u64 w = x1; w; w &= w - 1) hxx ^= c_hs[64 + __ffsll((long long)w) - 1];
-            // lanes test 32 alpha singles at a time; the adjacent ones present in
-            // the table are then processed one by one by the whole warp
-            for (int c0 = 0; c0 < combos; c0 += 32) {
-                const int cidx = c0 + lane;
-                int p = 0, q = 0;
-                int32_t g2 = -1;
-                if (cidx < combos) {
-                    p = nth_set(a, cidx / nva);
-                    q = nth_set(va, cidx % nva);
-                    g2 = alpha_lookup(T, a ^ (1ULL << p) ^ (1ULL << q));
-                    ++c_cand;
+        // ---- (i) same beta string: x' = (a'', b), a'' in A(b);  (ii) same alpha string
+        for (int ph = 0; ph < 2; ++ph) {
+            if (!(phase_mask & (2 << ph))) continue;
+            const int32_t g = ph == 0 ? T.gb_of[i] : T.ga_of[i];
+            const int32_t *off = ph == 0 ? T.offB : T.offA;
+            const u64 *lst = ph == 0 ? T.listB_a : T.listA_b;
+            const int32_t *lidx = ph == 0 ? T.listB_idx : T.listA_idx;
+            const u64 *str = ph == 0 ? T.sa : T.sb;          // the varying string of an entry
+            const u64 mine = ph == 0 ? a : b;
+            const int32_t jb = off[g], je = off[g + 1];
+            if (je - jb <= T.thr_double) {
+                for (int32_t j0 = jb; j0 < je; j0 += 128) {
+                    u64 v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int32_t j = j0 + 32 * u + lane;
+                        v[u] = j < je ? __ldg(lst + j) : mine;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int32_t j = j0 + 32 * u + lane;
+                        const u64 d = mine ^ v[u];
+                        const int c = __popcll(d);
+                        int32_t k = -1;
+                        if ((c == 2 || c == 4) && 2 * __popcll(mine & d) == c) k = same_spin_group(S, ph, d, c);
+                        c_cand += j < je;
+                        push(k, k >= 0 ? __ldg(lidx + j) : 0);
+                    }
                 }
-                unsigned ball = __ballot_sync(0xffffffffu, g2 >= 0);
-                while (ball) {
-                    const int src = __ffs(ball) - 1;
-                    ball &= ball - 1;
-                    const int pp = __shfl_sync(0xffffffffu, p, src);
-                    const int qq = __shfl_sync(0xffffffffu, q, src);
-                    const int32_t gg = __shfl_sync(0xffffffffu, g2, src);
-                    const int32_t *abk = S.ab_k + pair_rank(min(pp, qq), max(pp, qq), S.n) * S.P;
-                    const int32_t jb = T.offA[gg], je = T.offA[gg + 1];
-                    if (je - jb <= SCAN_LIMIT) {
-                        for (int32_t j = jb + lane; j < je; j += 32) {
-                            const u64 d = b ^ __ldg(T.listA_b + j);
-                            ++c_cand;
-                            if (__popcll(d) != 2 || __popcll(b & d) != 1) continue;
-                            const int r1 = __ffsll((long long)d) - 1;
-                            const int r2 = 63 - __clzll((long long)d);
-                            const int32_t k = __ldg(abk + pair_rank(r1, r2, S.n));
-                            if (k < 0) continue;
-                            ++c_hit;
-                            add(group_value1(G, k, x0, x1, c_str), __ldg(T.listA_idx + j));
+            } else {
+                // heavy group: 1-deletion (singles) and 2-deletion (doubles) probes
+                const int no = __popcll(mine);
+                const int ntask = no + no * (no - 1) / 2;
+                const int tag1 = ph == 0 ? 2 : 0;
+                for (int t0 = 0; t0 < ntask; t0 += 32) {
+                    const int t = t0 + lane;
+                    const bool live = t < ntask;
+                    u64 key = 0;
+                    uint32_t meta = 0;
+                    int want = 2;
+                    if (live) {
+                        const uint8_t *occ = ph == 0 ? occA : occB;
+                        if (t < no) {
+                            key = mine ^ (1ULL << occ[t]);
+                            meta = mm_meta(tag1, g);
+                        } else {
+                            int i1, i2;
+                            nth_pair(t - no, i1, i2);
+                            const int p1 = occ[i1], p2 = occ[i2];
+                            key = mine ^ (1ULL << p1) ^ (1ULL << p2);
+                            meta = mm_meta(tag1 + 1, g);
+                            want = 4;
                         }
-                    } else {
-                        // long list: probe each beta single of b in the full-key hash
-                        u64 u0 = 0, u1 = 0;
-                        spread_bit(pp, 0, u0, u1);
-                        spread_bit(qq, 0, u0, u1);
-                        const u64 hu = hxx ^ c_hs[2 * pp] ^ c_hs[2 * qq];
-                        for (int cb = lane; cb < bsingles; cb += 32) {
-                            const int r1 = nth_set(b, cb / nvb), r2 = nth_set(vb, cb % nvb);
-                            const int32_t k = __ldg(abk + pair_rank(min(r1, r2), max(r1, r2), S.n));
-                            ++c_cand;
-                            if (k < 0) continue;
-                            u64 w0 = u0, w1 = u1;
-                            spread_bit(r1, 1, w0, w1);
-                            spread_bit(r2, 1, w0, w1);
-                            const int64_t idx = probe_key(T, hu ^ c_hs[2 * r1 + 1] ^ c_hs[2 * r2 + 1], x0 ^ w0, x1 ^ w1);
-                            if (idx < 0) continue;
-                            ++c_hit;
-                            add(group_value1(G, k, x0, x1, c_str), idx);
+                        ++c_cand;
+                    }
+                    int32_t mb = 0, me = 0;
+                    if (live) mm_find(T, key, meta, mb, me);
+                    unsigned ball = __ballot_sync(0xffffffffu, me > mb);
+                    while (ball) {                       // matches of each probing lane, warp-wide
+                        const int src = __ffs(ball) - 1;
+                        ball &= ball - 1;
+                        const int32_t sb0 = __shfl_sync(0xffffffffu, mb, src);
+                        const int32_t se0 = __shfl_sync(0xffffffffu, me, src);
+                        const int swant = __shfl_sync(0xffffffffu, want, src);
+                        for (int32_t m0 = sb0; m0 < se0; m0 += 32) {
+                            const int32_t mj = m0 + lane;
+                            int32_t k = -1, idx = 0;
+                            if (mj < se0) {
+                                idx = __ldg(T.mm_val + mj);
+                                const u64 d = mine ^ __ldg(T.mm_str + mj);
+                                if (__popcll(d) == swant) k = same_spin_group(S, ph, d, swant);
+                            }
+                            push(k, idx);
                         }
                     }
                 }
             }
         }
+        // ---- (iii) alpha single u x beta single v
+        if (phase_mask & 8) {
+            const u64 va = ~a & nmask, vb = ~b & nmask;
+            const int noa = __popcll(a), nva = __popcll(va);
+            const int nob = __popcll(b), nvb = __popcll(vb);
+            const int combos = noa * nva;
+            (void)nob;
+            (void)nvb;
+            for (int c0 = 0; c0 < combos; c0 += 32) {
+                const int cidx = c0 + lane;
+                int p = 0, qo = 0;
+                int32_t g2 = -1;
+                if (cidx < combos) {
+                    p = occA[cidx / nva];
+                    qo = virA[cidx % nva];
+                    g2 = alpha_lookup(T, a ^ (1ULL << p) ^ (1ULL << qo));
+                    ++c_cand;
+                }
+                // list ranges of the adjacent alpha strings, prefetched per lane
+                int32_t ljb = 0, llen = 0;
+                if (g2 >= 0) {
+                    ljb = __ldg(T.offA + g2);
+                    llen = __ldg(T.offA + g2 + 1) - ljb;
+                }
+                const bool heavy = g2 >= 0 && llen > T.thr_single;
+                const int32_t ll = (g2 >= 0 && !heavy) ? llen : 0;
+                const int32_t urank = g2 >= 0 ? (int32_t)pair_rank(min(p, qo), max(p, qo), S.n) : 0;
+                int32_t incl = ll;                       // warp prefix sum of the light list lengths
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                const int32_t excl = incl - ll;
+                const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                // flattened scan of all light lists of this chunk: 128 entries per warp step
+                for (int32_t f0 = 0; f0 < total; f0 += 128) {
+                    u64 v[4];
+                    int32_t jj[4], ur[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int32_t f = f0 + 32 * u + lane;
+                        int lo = 0;
+#pragma unroll
+                        for (int st = 16; st; st >>= 1) {
+                            const int c = lo + st;
+                            const int32_t ex = __shfl_sync(0xffffffffu, excl, c & 31);
+                            if (c < 32 && ex <= f) lo = c;
+                        }
+                        const int32_t ob = __shfl_sync(0xffffffffu, ljb, lo);
+                        const int32_t oe = __shfl_sync(0xffffffffu, excl, lo);
+                        ur[u] = __shfl_sync(0xffffffffu, urank, lo);
+                        jj[u] = ob + (f - oe);
+                        v[u] = f < total ? __ldg(T.listA_b + jj[u]) : b;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const u64 d = b ^ v[u];
+                        int32_t k = -1;
+                        if (__popcll(d) == 2 && __popcll(b & d) == 1) {
+                            const int r1 = __ffsll((long long)d) - 1;
+                            const int r2 = 63 - __clzll((long long)d);
+                            k = __ldg(S.ab_k + (int64_t)ur[u] * S.P + pair_rank(r1, r2, S.n));
+                        }
+                        c_cand += (f0 + 32 * u + lane) < total;
+                        push(k, k >= 0 ? __ldg(T.listA_idx + jj[u]) : 0);
+                    }
+                }
+                // heavy adjacent alpha strings: multimap probes, one at a time
+                unsigned ball = __ballot_sync(0xffffffffu, heavy);
+                while (ball) {
+                    const int src = __ffs(ball) - 1;
+                    ball &= ball - 1;
+                    const int pp = __shfl_sync(0xffffffffu, p, src);
+                    const int qq = __shfl_sync(0xffffffffu, qo, src);
+                    const int32_t gg = __shfl_sync(0xffffffffu, g2, src);
+                    const int32_t *abk = S.ab_k + pair_rank(min(pp, qq), max(pp, qq), S.n) * S.P;
+                    {
+                        // heavy alpha group a': probe (a', b - e_r) deletions of b
+                        const int nob1 = __popcll(b);
+                        const uint32_t meta = mm_meta(0, gg);
+                        for (int t0 = 0; t0 < nob1; t0 += 32) {
+                            const int t = t0 + lane;
+                            int32_t mb = 0, me = 0;
+                            if (t < nob1) {
+                                mm_find(T, b ^ (1ULL << occB[t]), meta, mb, me);
+                                ++c_cand;
+                            }
+                            unsigned ball2 = __ballot_sync(0xffffffffu, me > mb);
+                            while (ball2) {
+                                const int src = __ffs(ball2) - 1;
+                                ball2 &= ball2 - 1;
+                                const int32_t sb0 = __shfl_sync(0xffffffffu, mb, src);
+                                const int32_t se0 = __shfl_sync(0xffffffffu, me, src);
+                                for (int32_t m0 = sb0; m0 < se0; m0 += 32) {
+                                    const int32_t mj = m0 + lane;
+                                    int32_t k = -1, idx = 0;
+                                    if (mj < se0) {
+                                        idx = __ldg(T.mm_val + mj);
+                                        const u64 d = b ^ __ldg(T.mm_str + mj);
+                                        if (d) {
+                                            const int r1 = __ffsll((long long)d) - 1;
+                                            const int r2 = 63 - __clzll((long long)d);
+                                            k = __ldg(abk + pair_rank(r1, r2, S.n));
+                                        }
+                                    }
+                                    push(k, idx);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        if (qn > 0) flush(qn);
         for (int o = 16; o; o >>= 1) {
             ar += __shfl_xor_sync(0xffffffffu, ar, o);
             ai += __shfl_xor_sync(0xffffffffu, ai, o);
@@ -390,6 +595,12 @@ __global__ void k_split(const ulonglong2 *keys, int64_t n, u64 *sa, u64 *sb, int
     }
 }
 
+__global__ void k_iota(int32_t *p, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = (int32_t)i;
+}
+
 __global__ void k_gather64(const u64 *src, const int32_t *perm, int64_t n, u64 *dst) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -424,6 +635,95 @@ __global__ void k_csr(const u64 *ksorted, const int32_t *perm, const int32_t *in
             }
         }
         if (j == n - 1) off[g + 1] = (int32_t)n;
+    }
+}
+
+// keys per entry (heavy groups only)
+__device__ __forceinline__ int mm_keys_of(int32_t la, int32_t lb, int na, int nb, int32_t thr_s, int32_t thr_d) {
+    int c = 0;
+    if (la > thr_s) c += nb;
+    if (la > thr_d) c += nb * (nb - 1) / 2;
+    if (lb > thr_s) c += na;
+    if (lb > thr_d) c += na * (na - 1) / 2;
+    return c;
+}
+
+__global__ void k_mm_count(const u64 *sa, const u64 *sb, const int32_t *ga_of, const int32_t *gb_of,
+                           const int32_t *offA, const int32_t *offB, int64_t n, int32_t thr_s, int32_t thr_d,
+                           int32_t *counts) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t la = offA[ga_of[e] + 1] - offA[ga_of[e]];
+        const int32_t lb = offB[gb_of[e] + 1] - offB[gb_of[e]];
+        counts[e] = mm_keys_of(la, lb, __popcll(sa[e]), __popcll(sb[e]), thr_s, thr_d);
+    }
+}
+
+// emit (key, meta, entry) at the entry's exclusive-scan offset (deterministic order)
+__global__ void k_mm_emit(const u64 *sa, const u64 *sb, const int32_t *ga_of, const int32_t *gb_of,
+                          const int32_t *offA, const int32_t *offB, int64_t n, int32_t thr_s, int32_t thr_d,
+                          const int64_t *eoff, u64 *K, uint32_t *M, int32_t *V, u64 *SV) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t ga = ga_of[e], gb = gb_of[e];
+        const int32_t la = offA[ga + 1] - offA[ga], lb = offB[gb + 1] - offB[gb];
+        int64_t o = eoff[e];
+        for (int side = 0; side < 2; ++side) {
+            const int32_t len = side == 0 ? la : lb;   // side 0: beta deletions keyed by alpha group
+            const u64 w = side == 0 ? sb[e] : sa[e];
+            const int32_t g = side == 0 ? ga : gb;
+            const int tag = side == 0 ? 0 : 2;
+            if (len <= thr_s) continue;
+            for (u64 m1 = w; m1; m1 &= m1 - 1) {
+                const u64 b1 = m1 & (~m1 + 1);
+                K[o] = w ^ b1; M[o] = mm_meta(tag, g); V[o] = (int32_t)e; SV[o] = w; ++o;
+            }
+            if (len > thr_d)
+                for (u64 m1 = w; m1; m1 &= m1 - 1) {
+                    const u64 b1 = m1 & (~m1 + 1);
+                    for (u64 m2 = m1 & (m1 - 1); m2; m2 &= m2 - 1) {
+                        const u64 b2 = m2 & (~m2 + 1);
+                        K[o] = w ^ b1 ^ b2; M[o] = mm_meta(tag + 1, g); V[o] = (int32_t)e; SV[o] = w; ++o;
+                    }
+                }
+        }
+    }
+}
+
+__global__ void k_gather32(const uint32_t *src, const int32_t *perm, int64_t n, uint32_t *dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[perm[i]];
+}
+
+__global__ void k_mm_heads(const u64 *K2, const uint32_t *M2, int64_t m, int32_t *flag) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
+         j += (int64_t)gridDim.x * blockDim.x)
+        flag[j] = (j == 0 || K2[j] != K2[j - 1] || M2[j] != M2[j - 1]) ? 1 : 0;
+}
+
+__global__ void k_mm_runs(const u64 *K2, const uint32_t *M2, const int32_t *P2, const int32_t *V, const u64 *SV,
+                          const int32_t *rid, int64_t m, int32_t *run_start, int32_t *val, u64 *str,
+                          ulonglong2 *slots, u64 mask) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        val[j] = V[P2[j]];
+        str[j] = SV[P2[j]];
+        const int32_t r = rid[j] - 1;
+        if (j == 0 || K2[j] != K2[j - 1] || M2[j] != M2[j - 1]) {
+            run_start[r] = (int32_t)j;
+            u64 s = mm_hash(K2[j], M2[j]) & mask;
+            while (true) {
+                uint32_t *w = reinterpret_cast<uint32_t *>(slots + s);
+                if (atomicCAS(w + 3, MM_EMPTY, (uint32_t)r) == MM_EMPTY) {
+                    slots[s].x = K2[j];
+                    w[2] = M2[j];
+                    break;
+                }
+                s = (s + 1) & mask;
+            }
+        }
+        if (j == m - 1) run_start[r + 1] = (int32_t)m;
     }
 }
 
@@ -503,6 +803,103 @@ void nnqs_spin_index_release(nnqs_ham h) {
     D.ab_k = nullptr;
 }
 
+namespace {
+int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, void *, size_t) {
+    const int g = grid_for(n, 256);
+    int64_t *eoff = nullptr;
+    int rc = cuda_check(cudaMallocAsync((void **)&eoff, 8 * (n + 1), st), "alloc mm offsets");
+    if (rc) return rc;
+    k_mm_count<<<g, 256, 0, st>>>(t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB, n, t->thr_single,
+                                  t->thr_double, counts);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, eoff, (int)n + 1, st);
+    void *stmp = nullptr;
+    cudaMemsetAsync(eoff + n, 0, 8, st);
+    rc = cuda_check(cudaMallocAsync(&stmp, tb, st), "alloc scan tmp");
+    if (rc) { cudaFreeAsync(eoff, st); return rc; }
+    // counts has n entries; scan n+1 with a zero appended (counts[n] read as 0)
+    int32_t *cz = nullptr;
+    cudaMallocAsync((void **)&cz, 4 * (n + 1), st);
+    cudaMemcpyAsync(cz, counts, 4 * n, cudaMemcpyDeviceToDevice, st);
+    cudaMemsetAsync(cz + n, 0, 4, st);
+    cub::DeviceScan::ExclusiveSum(stmp, tb, cz, eoff, (int)n + 1, st);
+    int64_t m = 0;
+    rc = cuda_check(cudaMemcpyAsync(&m, eoff + n, 8, cudaMemcpyDeviceToHost, st), "read mm size");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
+    cudaFreeAsync(stmp, st);
+    cudaFreeAsync(cz, st);
+    if (rc || m == 0) {
+        cudaFreeAsync(eoff, st);
+        if (!rc) {   // empty multimap: one empty slot
+            rc = cuda_check(cudaMallocAsync(&t->mm_buf, 128, st), "alloc mm");
+            if (rc) return rc;
+            t->mm = t->mm_buf;
+            t->mm_mask = 0;
+            t->mm_run = (int32_t *)((char *)t->mm_buf + 16);
+            t->mm_val = (int32_t *)((char *)t->mm_buf + 32);
+            t->mm_str = (u64 *)((char *)t->mm_buf + 48);
+            cudaMemsetAsync(t->mm, 0xFF, 16, st);
+        }
+        return rc;
+    }
+    if (m >= (1LL << 31)) { cudaFreeAsync(eoff, st); return nnqs_set_error(NNQS_E_SIZE, "multimap too large"); }
+    // scratch for the sort
+    auto r16 = [](size_t b) { return (b + 15) & ~size_t(15); };
+    size_t t1 = 0, t2 = 0, t3 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, (const u64 *)nullptr, (u64 *)nullptr, (const int32_t *)nullptr,
+                                    (int32_t *)nullptr, (int)m, 0, 64, st);
+    cub::DeviceRadixSort::SortPairs(nullptr, t2, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (const int32_t *)nullptr, (int32_t *)nullptr, (int)m, 0, 32, st);
+    cub::DeviceScan::InclusiveSum(nullptr, t3, (const int32_t *)nullptr, (int32_t *)nullptr, (int)m, st);
+    const size_t ctb = std::max(t1, std::max(t2, t3));
+    const size_t sbytes = 4 * r16(8 * m) + 3 * r16(4 * m) + 4 * r16(4 * m) + r16(ctb) + 64;
+    char *sc = nullptr;
+    rc = cuda_check(cudaMallocAsync((void **)&sc, sbytes, st), "alloc mm scratch");
+    if (rc) { cudaFreeAsync(eoff, st); return rc; }
+    char *sp = sc;
+    auto take = [&](size_t b) { char *p = sp; sp += r16(b); return p; };
+    u64 *K = (u64 *)take(8 * m), *K1 = (u64 *)take(8 * m), *K2 = (u64 *)take(8 * m), *SV = (u64 *)take(8 * m);
+    uint32_t *M = (uint32_t *)take(4 * m), *M1 = (uint32_t *)take(4 * m), *M2 = (uint32_t *)take(4 * m);
+    int32_t *V = (int32_t *)take(4 * m), *io = (int32_t *)take(4 * m), *P1 = (int32_t *)take(4 * m),
+            *P2 = (int32_t *)take(4 * m);
+    void *ct = take(ctb);
+    const int gm = grid_for(m, 256);
+    k_mm_emit<<<g, 256, 0, st>>>(t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB, n, t->thr_single,
+                                 t->thr_double, eoff, K, M, V, SV);
+    k_iota<<<gm, 256, 0, st>>>(io, m);
+    size_t tb1 = ctb;
+    cub::DeviceRadixSort::SortPairs(ct, tb1, K, K1, io, P1, (int)m, 0, 64, st);
+    k_gather32<<<gm, 256, 0, st>>>(M, P1, m, M1);
+    tb1 = ctb;
+    cub::DeviceRadixSort::SortPairs(ct, tb1, M1, M2, P1, P2, (int)m, 0, 32, st);
+    k_gather64<<<gm, 256, 0, st>>>(K, P2, m, K2);
+    k_mm_heads<<<gm, 256, 0, st>>>(K2, M2, m, io);        // io reused as head flags
+    tb1 = ctb;
+    cub::DeviceScan::InclusiveSum(ct, tb1, io, P1, (int)m, st);   // P1 reused as run ids (1-based)
+    int32_t nruns = 0;
+    rc = cuda_check(cudaMemcpyAsync(&nruns, P1 + m - 1, 4, cudaMemcpyDeviceToHost, st), "read runs");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
+    if (rc) { cudaFreeAsync(sc, st); cudaFreeAsync(eoff, st); return rc; }
+    u64 slots = 2;
+    while (slots < 2 * (u64)nruns) slots <<= 1;
+    const size_t pbytes = r16(16 * slots) + r16(4 * ((size_t)nruns + 1)) + r16(4 * m) + r16(8 * m);
+    rc = cuda_check(cudaMallocAsync(&t->mm_buf, pbytes, st), "alloc multimap");
+    if (rc) { cudaFreeAsync(sc, st); cudaFreeAsync(eoff, st); return rc; }
+    t->mm = t->mm_buf;
+    t->mm_mask = slots - 1;
+    t->mm_run = (int32_t *)((char *)t->mm_buf + r16(16 * slots));
+    t->mm_val = (int32_t *)((char *)t->mm_run + r16(4 * ((size_t)nruns + 1)));
+    t->mm_str = (u64 *)((char *)t->mm_val + r16(4 * m));
+    t->bytes += (int64_t)pbytes;
+    cudaMemsetAsync(t->mm, 0xFF, 16 * slots, st);
+    k_mm_runs<<<gm, 256, 0, st>>>(K2, M2, P2, V, SV, P1, m, t->mm_run, t->mm_val, t->mm_str, (ulonglong2 *)t->mm,
+                                  t->mm_mask);
+    cudaFreeAsync(sc, st);
+    cudaFreeAsync(eoff, st);
+    return cuda_check(cudaGetLastError(), "multimap kernels");
+}
+}  // namespace
+
 int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
     if (!h->spin.ok || t->mode != 0 || t->n == 0) return NNQS_OK;
     cudaStream_t st = (cudaStream_t)stream;
@@ -572,6 +969,13 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
             k_csr<<<g, 256, 0, st>>>(k1, perm2, incl, n, t->sa, t->offB, t->gb_of, t->listB_a, t->listB_idx,
                                      nullptr, nullptr, 0);
     }
+    // deletion multimap for heavy groups (sorted CSR + unique-key hash)
+    t->thr_single = 192;
+    t->thr_double = 4096;
+    if (const char *e = std::getenv("NNQS_THR_SINGLE")) t->thr_single = std::atoi(e);   // tuning only
+    if (const char *e = std::getenv("NNQS_THR_DOUBLE")) t->thr_double = std::atoi(e);
+    rc = build_multimap(t, n, st, flags, ctmp, tmp);
+    if (rc) { cudaFreeAsync(scratch, st); return rc; }
     cudaFreeAsync(scratch, st);
     rc = cuda_check(cudaGetLastError(), "spin index kernels");
     if (rc) return rc;
@@ -581,6 +985,8 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
 
 void nnqs_table_release_spin(nnqs_table t) {
     if (t->spin_buf) cudaFreeAsync(t->spin_buf, (cudaStream_t)t->stream);
+    if (t->mm_buf) cudaFreeAsync(t->mm_buf, (cudaStream_t)t->stream);
+    t->mm = t->mm_buf = nullptr;
     t->spin_buf = nullptr;
     t->spin_ready = false;
 }
@@ -593,7 +999,9 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
     GroupView gv{D.goff, (const ulonglong2 *)D.tz, D.td};
     TabSpin tv{t->n, (const ulonglong2 *)t->keys, (const double2 *)t->logpsi, (const double2 *)t->psi_hat,
                t->slots, t->bucket_mask, t->shift_key, t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB,
-               t->listA_b, t->listB_a, t->listA_idx, t->listB_idx, t->ah_keys, t->ah_vals, t->ah_mask};
+               t->listA_b, t->listB_a, t->listA_idx, t->listB_idx, t->ah_keys, t->ah_vals, t->ah_mask,
+               (const ulonglong2 *)t->mm, t->mm_mask, t->mm_run, t->mm_val, t->mm_str, t->thr_single,
+               t->thr_double};
     const int64_t threads = n_rows * 32;
     int g = (int)std::min<int64_t>((threads + 255) / 256, 148 * 64);
     if (g < 1) g = 1;
@@ -602,7 +1010,12 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
     if (rc) return rc;
     // stats[0] = row-group pairs resolved (the literal loop's R * K')
     const unsigned long long pairs = (unsigned long long)n_rows * (unsigned long long)h->n_groups;
+    static int phase_mask = -1;
+    if (phase_mask < 0) {
+        const char *e = std::getenv("NNQS_PHASE_MASK");   // debug / profiling only
+        phase_mask = e ? std::atoi(e) : 15;
+    }
     k_eloc_spin<<<g, 256, 0, st>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc, (unsigned long long *)stats,
-                                   pairs);
+                                   pairs, phase_mask);
     return cuda_check(cudaGetLastError(), "structured local energy launch");
 }
