@@ -35,8 +35,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
             continue
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         if src.endswith(".cu"):
+            extra = os.environ.get("NNQS_NVCC_DEFINES", "").split()   # tuning experiments only
             cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-                   "-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj]
+                   "-Xptxas", "-v" if verbose else "-O3", *extra, "-c", src, "-o", obj]
         else:
             cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-fopenmp", "-march=x86-64-v2",
                    "-I/usr/local/cuda/include", "-c", src, "-o", obj]

@@ -232,6 +232,9 @@ __device__ __forceinline__ void nth_pair(int c, int &i, int &j) {
 
 #define SCAN_LIMIT 8192
 #define WARPS_PER_BLOCK 8
+#ifndef NNQS_SPIN_MINB
+#define NNQS_SPIN_MINB 3
+#endif
 #define QCAP 64
 
 // one warp per row; rows are table entries [row_begin, row_begin + n_rows).
@@ -239,7 +242,7 @@ __device__ __forceinline__ void nth_pair(int c, int &i, int &j) {
 // string lists; hits (group k, table index) go to a per-warp queue and are
 // evaluated 32 at a time, one per lane (slot s -> lane s mod 32, so the
 // summation order of a row is fixed by the row and the table).
-__global__ void __launch_bounds__(256, 2) k_eloc_spin(SpinView S, GroupView G, TabSpin T, int64_t row_begin,
+__global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, GroupView G, TabSpin T, int64_t row_begin,
                                                    int64_t n_rows, double2 *out,
                                                    unsigned long long *stats, unsigned long long pairs,
                                                    int phase_mask) {
