@@ -117,6 +117,9 @@ struct nnqs_table_s {
     u64 *mm_str = nullptr;                     // ... and the entry's varying string
     void *mm_buf = nullptr;
     int32_t thr_single = 0, thr_double = 0;    // list-length thresholds
+    int32_t thr_rowheavy = 0;                  // alpha groups with more rows: entry-driven phase (iii)
+    int32_t *heavy_groups = nullptr;           // [n_heavy] those alpha group ids (device)
+    int n_heavy = 0;
 };
 
 int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream);

@@ -58,13 +58,12 @@ inline int grid_for(int64_t n, int block) {
     return (int)g;
 }
 
-__host__ __device__ __forceinline__ int64_t pair_rank(int p, int q, int n) {   // p < q
-    return (int64_t)p * (2 * n - p - 1) / 2 + (q - p - 1);
+__host__ __device__ __forceinline__ int pair_rank(int p, int q, int n) {   // p < q < n <= 64
+    return ((p * (2 * n - p - 1)) >> 1) + (q - p - 1);
 }
 
-__host__ __device__ __forceinline__ int64_t quad_rank(int p1, int p2, int p3, int p4) {  // colex, p1<p2<p3<p4
-    return (int64_t)p1 + (int64_t)p2 * (p2 - 1) / 2 + (int64_t)p3 * (p3 - 1) * (p3 - 2) / 6 +
-           (int64_t)p4 * (p4 - 1) * (p4 - 2) * (p4 - 3) / 24;
+__host__ __device__ __forceinline__ int quad_rank(int p1, int p2, int p3, int p4) {  // colex, p1<p2<p3<p4<64
+    return p1 + ((p2 * (p2 - 1)) >> 1) + (p3 * (p3 - 1) * (p3 - 2)) / 6 + (p4 * (p4 - 1) * (p4 - 2) * (p4 - 3)) / 24;
 }
 
 __host__ __device__ __forceinline__ u64 mix64(u64 z) {
@@ -230,6 +229,68 @@ __device__ __forceinline__ void nth_pair(int c, int &i, int &j) {
     i = c - j * (j - 1) / 2;
 }
 
+// Evaluate the first cnt queued hits (lane l takes slot l), add their
+// contributions H * psi(x') to the lane accumulators, and shift the queue.
+// Out of line: it is reached from every candidate site, and inlining it there
+// overflowed the instruction cache.
+__device__ __noinline__ void flush_queue(const GroupView &G, const TabSpin &T, int2 *q, int qn, int cnt, u64 x0,
+                                         u64 x1, double2 lx, bool direct, double &ar, double &ai,
+                                         unsigned long long &c_hit, unsigned long long &c_str) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    int2 e = make_int2(-1, 0);
+    uint32_t gb0 = 0, ge0 = 0;
+    if (lane < cnt) {
+        e = q[lane];
+        gb0 = __ldg(G.goff + e.x);
+        ge0 = __ldg(G.goff + e.x + 1);
+        ++c_hit;
+    }
+    auto add = [&](double hv, int64_t idx) {
+        double2 ps;
+        if (!direct) {
+            ps = __ldg(T.psi_hat + idx);
+        } else {
+            const double2 l = T.logpsi[idx];
+            const double m = exp(l.x - lx.x);
+            double sn, cs;
+            sincos(l.y - lx.y, &sn, &cs);
+            ps = make_double2(m * cs, m * sn);
+        }
+        ar = fma(hv, ps.x, ar);
+        ai = fma(hv, ps.y, ai);
+    };
+    const bool big = lane < cnt && ge0 - gb0 > 32;
+    if (lane < cnt && !big) {
+        double hv = 0.0;
+        for (uint32_t i = gb0; i < ge0; ++i) {
+            const ulonglong2 Z = __ldg(G.tz + i);
+            hv += flip_sign2(__ldg(G.td + i), (__popcll(x0 & Z.x) + __popcll(x1 & Z.y)) & 1);
+        }
+        c_str += ge0 - gb0;
+        add(hv, e.y);
+    }
+    unsigned bigs = __ballot_sync(0xffffffffu, big);
+    while (bigs) {                               // long groups: whole warp, fixed reduction
+        const int src = __ffs(bigs) - 1;
+        bigs &= bigs - 1;
+        const uint32_t b1 = __shfl_sync(0xffffffffu, gb0, src), e1 = __shfl_sync(0xffffffffu, ge0, src);
+        double hv = 0.0;
+        for (uint32_t t = b1 + lane; t < e1; t += 32) {
+            const ulonglong2 Z = __ldg(G.tz + t);
+            hv += flip_sign2(__ldg(G.td + t), (__popcll(x0 & Z.x) + __popcll(x1 & Z.y)) & 1);
+        }
+        for (int o = 16; o; o >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, o);
+        if (lane == src) {
+            add(hv, e.y);
+            c_str += e1 - b1;
+        }
+    }
+    __syncwarp();
+    if (lane < qn - cnt) q[lane] = q[lane + cnt];
+    __syncwarp();
+}
+
 #define SCAN_LIMIT 8192
 #define WARPS_PER_BLOCK 8
 #ifndef NNQS_SPIN_MINB
@@ -245,7 +306,7 @@ __device__ __forceinline__ void nth_pair(int c, int &i, int &j) {
 __global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, GroupView G, TabSpin T, int64_t row_begin,
                                                    int64_t n_rows, double2 *out,
                                                    unsigned long long *stats, unsigned long long pairs,
-                                                   int phase_mask) {
+                                                   int phase_mask, const double2 *acc_heavy, int32_t thr_rowheavy) {
     __shared__ int2 s_q[WARPS_PER_BLOCK][QCAP];
     __shared__ uint8_t s_orb[WARPS_PER_BLOCK][4][64];   // occ(a), vir(a), occ(b), vir(b) of the row
     if (stats && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(stats, pairs);
@@ -298,36 +359,7 @@ __global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, G
         };
         int qn = 0;                                  // warp-uniform queue length
         auto flush = [&](int cnt) {                  // lanes < cnt evaluate q[lane]
-            __syncwarp();
-            int2 e = make_int2(-1, 0);
-            uint32_t gb0 = 0, ge0 = 0;
-            if (lane < cnt) {
-                e = q[lane];
-                gb0 = __ldg(G.goff + e.x);
-                ge0 = __ldg(G.goff + e.x + 1);
-                ++c_hit;
-            }
-            const bool big = lane < cnt && ge0 - gb0 > 32;
-            if (lane < cnt && !big) add(group_value1(G, e.x, x0, x1, c_str), e.y);
-            unsigned bigs = __ballot_sync(0xffffffffu, big);
-            while (bigs) {                               // long groups: whole warp, fixed reduction
-                const int src = __ffs(bigs) - 1;
-                bigs &= bigs - 1;
-                const uint32_t b1 = __shfl_sync(0xffffffffu, gb0, src), e1 = __shfl_sync(0xffffffffu, ge0, src);
-                double hv = 0.0;
-                for (uint32_t t = b1 + lane; t < e1; t += 32) {
-                    const ulonglong2 Z = __ldg(G.tz + t);
-                    hv += flip_sign2(__ldg(G.td + t), (__popcll(x0 & Z.x) + __popcll(x1 & Z.y)) & 1);
-                }
-                for (int o = 16; o; o >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, o);
-                if (lane == src) {
-                    add(hv, e.y);
-                    c_str += e1 - b1;
-                }
-            }
-            __syncwarp();
-            if (lane < qn - cnt) q[lane] = q[lane + cnt];
-            __syncwarp();
+            flush_queue(G, T, q, qn, cnt, x0, x1, lx, direct, ar, ai, c_hit, c_str);
             qn -= cnt;
         };
         auto push = [&](int32_t k, int32_t idx) {    // all lanes; k < 0 = no hit
@@ -431,7 +463,14 @@ __global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, G
             }
         }
         // ---- (iii) alpha single u x beta single v
-        if (phase_mask & 8) {
+        const int32_t ga_row = T.ga_of[i];
+        const bool row_heavy = acc_heavy && (T.offA[ga_row + 1] - T.offA[ga_row] > thr_rowheavy);
+        if (row_heavy && lane == 0) {              // precomputed by the entry-driven join
+            const double2 h = acc_heavy[r];
+            ar += h.x;
+            ai += h.y;
+        }
+        if ((phase_mask & 8) && !row_heavy) {
             const u64 va = ~a & nmask, vb = ~b & nmask;
             const int noa = __popcll(a), nva = __popcll(va);
             const int nob = __popcll(b), nvb = __popcll(vb);
@@ -466,7 +505,7 @@ __global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, G
                 const int32_t excl = incl - ll;
                 const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
                 // flattened scan of all light lists of this chunk: 128 entries per warp step
-                for (int32_t f0 = 0; f0 < total; f0 += 128) {
+                for (int32_t f0 = 0; f0 < ((phase_mask & 16) ? 0 : total); f0 += 128) {
                     u64 v[4];
                     int32_t jj[4], ur[4];
 #pragma unroll
@@ -499,7 +538,7 @@ __global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, G
                     }
                 }
                 // heavy adjacent alpha strings: multimap probes, one at a time
-                unsigned ball = __ballot_sync(0xffffffffu, heavy);
+                unsigned ball = __ballot_sync(0xffffffffu, heavy && !(phase_mask & 32));
                 while (ball) {
                     const int src = __ffs(ball) - 1;
                     ball &= ball - 1;
@@ -727,6 +766,139 @@ __global__ void k_mm_runs(const u64 *K2, const uint32_t *M2, const int32_t *P2, 
             }
         }
         if (j == m - 1) run_start[r + 1] = (int32_t)m;
+    }
+}
+
+// ---------------------------------------------- entry-driven phase (iii) join
+// For an alpha group g with very many rows (the Hartree-Fock alpha string pairs
+// with ~10^5 rows at 120 qubits), phase (iii) is evaluated from the neighbour
+// side: every entry (a', b'') of every adjacent alpha string a' = a ^ u probes
+// the 1-deletions b'' - e_s in g's multimap (tag 0) and finds the rows (a, b)
+// with b - e_r = b'' - e_s.  Hits are emitted as (row, x' index) keys, sorted,
+// and summed per row in that order (k_hj_eval), so the result is deterministic.
+__global__ void __launch_bounds__(256) k_hj_emit(SpinView S, TabSpin T, const int32_t *heavy_groups, int n_heavy,
+                                                 int64_t row_begin, int64_t row_end, unsigned long long *counter,
+                                                 u64 *keys_out, int64_t cap, unsigned long long *stats) {
+    // block -> (heavy group, alpha single); threads -> entries of the neighbour's list
+    const int hg = blockIdx.x >> 10;
+    const int cidx = blockIdx.x & 1023;
+    if (hg >= n_heavy) return;
+    const u64 nmask = S.n >= 64 ? ~0ULL : ((1ULL << S.n) - 1);
+    const int32_t g = heavy_groups[hg];
+    const u64 a = T.sa[T.listA_idx[T.offA[g]]];
+    const u64 va = ~a & nmask;
+    const int nva = __popcll(va);
+    if (cidx >= __popcll(a) * nva) return;
+    const int p = nth_set(a, cidx / nva), q = nth_set(va, cidx % nva);
+    const int32_t g2 = alpha_lookup(T, a ^ (1ULL << p) ^ (1ULL << q));
+    if (g2 < 0) return;
+    const int32_t *abk = S.ab_k + pair_rank(min(p, q), max(p, q), S.n) * S.P;
+    const uint32_t meta = mm_meta(0, g);
+    const int32_t jb = T.offA[g2], je = T.offA[g2 + 1];
+    unsigned long long probes = 0;
+    for (int32_t j = jb + threadIdx.x; j < je; j += blockDim.x) {
+        const u64 b2 = T.listA_b[j];
+        const int32_t idx2 = T.listA_idx[j];
+        for (u64 m1 = b2; m1; m1 &= m1 - 1) {
+            int32_t mb, me;
+            mm_find(T, b2 ^ (m1 & (~m1 + 1)), meta, mb, me);
+            ++probes;
+            for (int32_t mj = mb; mj < me; ++mj) {
+                const int32_t e = T.mm_val[mj];
+                if (e < row_begin || e >= row_end) continue;
+                const u64 d = T.mm_str[mj] ^ b2;
+                if (!d) continue;
+                const int r1 = __ffsll((long long)d) - 1, r2 = 63 - __clzll((long long)d);
+                if (abk[pair_rank(r1, r2, S.n)] < 0) continue;
+                const unsigned long long slot = atomicAdd(counter, 1ULL);
+                if ((int64_t)slot < cap) keys_out[slot] = ((u64)(e - row_begin) << 32) | (u64)(uint32_t)idx2;
+            }
+        }
+    }
+    if (stats) {
+        for (int o = 16; o; o >>= 1) probes += __shfl_xor_sync(0xffffffffu, probes, o);
+        if ((threadIdx.x & 31) == 0) atomicAdd(stats + 1, probes);
+    }
+}
+
+__device__ __forceinline__ int64_t lower_bound_u64(const u64 *a, int64_t n, u64 v) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// one warp per row of the heavy groups: sum its sorted hits (fixed lane order)
+__global__ void k_hj_eval(SpinView S, GroupView G, TabSpin T, const int32_t *heavy_groups, int n_heavy,
+                          int64_t row_begin, int64_t row_end, const u64 *keys, int64_t m, double2 *acc,
+                          unsigned long long *stats) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const double s = dkey_inv2(*T.shift_key);
+    unsigned long long c_hit = 0, c_str = 0;
+    for (int hg = 0; hg < n_heavy; ++hg) {
+        const int32_t g = heavy_groups[hg];
+        const int32_t rb = T.offA[g], re = T.offA[g + 1];
+        for (int64_t t = warp; t < re - rb; t += nwarps) {
+            const int32_t e = T.listA_idx[rb + t];
+            if (e < row_begin || e >= row_end) continue;
+            const u64 rloc = (u64)(e - row_begin);
+            const int64_t kb = lower_bound_u64(keys, m, rloc << 32);
+            const int64_t ke = lower_bound_u64(keys, m, (rloc + 1) << 32);
+            const ulonglong2 xk = T.keys[e];
+            const u64 a = T.sa[e], b = T.sb[e];
+            const double2 lx = T.logpsi[e];
+            const bool direct = (lx.x - s) < -600.0;
+            double ar = 0.0, ai = 0.0;
+            for (int64_t j = kb + lane; j < ke; j += 32) {
+                const int32_t idx = (int32_t)(uint32_t)keys[j];
+                const u64 du = a ^ T.sa[idx], dv = b ^ T.sb[idx];
+                const int p1 = __ffsll((long long)du) - 1, p2 = 63 - __clzll((long long)du);
+                const int r1 = __ffsll((long long)dv) - 1, r2 = 63 - __clzll((long long)dv);
+                const int32_t k = S.ab_k[pair_rank(p1, p2, S.n) * S.P + pair_rank(r1, r2, S.n)];
+                const double hv = group_value1(G, k, xk.x, xk.y, c_str);
+                double2 ps;
+                if (!direct) {
+                    ps = T.psi_hat[idx];
+                } else {
+                    const double2 l = T.logpsi[idx];
+                    const double mg = exp(l.x - lx.x);
+                    double sn, cs;
+                    sincos(l.y - lx.y, &sn, &cs);
+                    ps = make_double2(mg * cs, mg * sn);
+                }
+                ar = fma(hv, ps.x, ar);
+                ai = fma(hv, ps.y, ai);
+                ++c_hit;
+            }
+            for (int o = 16; o; o >>= 1) {
+                ar += __shfl_xor_sync(0xffffffffu, ar, o);
+                ai += __shfl_xor_sync(0xffffffffu, ai, o);
+            }
+            if (lane == 0) acc[rloc] = make_double2(ar, ai);
+        }
+    }
+    if (stats) {
+        for (int o = 16; o; o >>= 1) {
+            c_hit += __shfl_xor_sync(0xffffffffu, c_hit, o);
+            c_str += __shfl_xor_sync(0xffffffffu, c_str, o);
+        }
+        if (lane == 0) {
+            atomicAdd(stats + 2, c_hit);
+            atomicAdd(stats + 3, c_str);
+        }
+    }
+}
+
+__global__ void k_find_heavy(const int32_t *listA_idx, const int32_t *ga_of, const int32_t *offA, int64_t n,
+                             int32_t thr, int32_t *out, int *count) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t g = ga_of[listA_idx[j]];
+        if (offA[g] == (int32_t)j && offA[g + 1] - offA[g] > thr) out[atomicAdd(count, 1)] = g;
     }
 }
 
@@ -979,6 +1151,31 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
     if (const char *e = std::getenv("NNQS_THR_DOUBLE")) t->thr_double = std::atoi(e);
     rc = build_multimap(t, n, st, flags, ctmp, tmp);
     if (rc) { cudaFreeAsync(scratch, st); return rc; }
+    t->thr_rowheavy = 16384;
+    if (const char *e = std::getenv("NNQS_THR_ROWHEAVY")) t->thr_rowheavy = std::atoi(e);   // tuning only
+    if (t->thr_rowheavy < t->thr_single) t->thr_rowheavy = t->thr_single;   // rows must be in the multimap
+    {
+        int *cnt_d = (int *)incl;   // scratch reuse
+        int32_t *hg = (int32_t *)perm1;
+        cudaMemsetAsync(cnt_d, 0, sizeof(int), st);
+        k_find_heavy<<<g, 256, 0, st>>>(t->listA_idx, t->ga_of, t->offA, n, t->thr_rowheavy, hg, cnt_d);
+        int nh = 0;
+        rc = cuda_check(cudaMemcpyAsync(&nh, cnt_d, sizeof(int), cudaMemcpyDeviceToHost, st), "read heavy");
+        if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
+        if (rc) { cudaFreeAsync(scratch, st); return rc; }
+        t->n_heavy = nh;
+        if (nh) {
+            rc = cuda_check(cudaMallocAsync((void **)&t->heavy_groups, 4 * nh, st), "alloc heavy");
+            if (rc) { cudaFreeAsync(scratch, st); return rc; }
+            // deterministic order of the heavy groups: sort the few ids on the host
+            std::vector<int32_t> ids(nh);
+            cudaMemcpyAsync(ids.data(), hg, 4 * nh, cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            std::sort(ids.begin(), ids.end());
+            cudaMemcpyAsync(t->heavy_groups, ids.data(), 4 * nh, cudaMemcpyHostToDevice, st);
+            cudaStreamSynchronize(st);
+        }
+    }
     cudaFreeAsync(scratch, st);
     rc = cuda_check(cudaGetLastError(), "spin index kernels");
     if (rc) return rc;
@@ -989,6 +1186,9 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
 void nnqs_table_release_spin(nnqs_table t) {
     if (t->spin_buf) cudaFreeAsync(t->spin_buf, (cudaStream_t)t->stream);
     if (t->mm_buf) cudaFreeAsync(t->mm_buf, (cudaStream_t)t->stream);
+    if (t->heavy_groups) cudaFreeAsync(t->heavy_groups, (cudaStream_t)t->stream);
+    t->heavy_groups = nullptr;
+    t->n_heavy = 0;
     t->mm = t->mm_buf = nullptr;
     t->spin_buf = nullptr;
     t->spin_ready = false;
@@ -1018,7 +1218,58 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
         const char *e = std::getenv("NNQS_PHASE_MASK");   // debug / profiling only
         phase_mask = e ? std::atoi(e) : 15;
     }
+    double2 *acc_heavy = nullptr;
+    u64 *hkeys = nullptr;
+    void *htmp = nullptr;
+    unsigned long long *hcnt = nullptr;
+    if (t->n_heavy > 0 && (phase_mask & 8)) {
+        const int64_t row_end = row_begin + n_rows;
+        rc = cuda_check(cudaMallocAsync((void **)&acc_heavy, 16 * n_rows + 16, st), "alloc acc_heavy");
+        if (!rc) rc = cuda_check(cudaMallocAsync((void **)&hcnt, 16, st), "alloc hj counter");
+        if (rc) return rc;
+        cudaMemsetAsync(acc_heavy, 0, 16 * n_rows, st);
+        cudaMemsetAsync(hcnt, 0, 16, st);
+        const int hgrid = t->n_heavy * 1024;
+        int64_t cap = std::max<int64_t>(1 << 20, std::min<int64_t>((int64_t)1 << 26, 64 * n_rows));
+        for (int attempt = 0; attempt < 2 && !rc; ++attempt) {
+            size_t tb = 0;
+            cub::DeviceRadixSort::SortKeys(nullptr, tb, (const u64 *)nullptr, (u64 *)nullptr, (int)cap, 0, 64, st);
+            rc = cuda_check(cudaMallocAsync((void **)&hkeys, 16 * cap + tb + 64, st), "alloc hj keys");
+            if (rc) break;
+            cudaMemsetAsync(hcnt, 0, 8, st);
+            k_hj_emit<<<hgrid, 256, 0, st>>>(sv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end, hcnt, hkeys,
+                                             cap, attempt == 0 ? (unsigned long long *)stats : nullptr);
+            unsigned long long m = 0;
+            rc = cuda_check(cudaMemcpyAsync(&m, hcnt, 8, cudaMemcpyDeviceToHost, st), "read hj count");
+            if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
+            if (rc) break;
+            if ((int64_t)m > cap) {              // buffer too small: size exactly and redo
+                cudaFreeAsync(hkeys, st);
+                hkeys = nullptr;
+                cap = (int64_t)m;
+                continue;
+            }
+            if (m) {
+                u64 *k2 = hkeys + cap;
+                htmp = (void *)(hkeys + 2 * cap);
+                tb = 0;
+                cub::DeviceRadixSort::SortKeys(nullptr, tb, (const u64 *)nullptr, (u64 *)nullptr, (int)m, 0, 64, st);
+                cub::DeviceRadixSort::SortKeys(htmp, tb, hkeys, k2, (int)m, 0, 64, st);
+                k_hj_eval<<<148 * 8, 256, 0, st>>>(sv, gv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end, k2,
+                                                   (int64_t)m, acc_heavy, (unsigned long long *)stats);
+            }
+            break;
+        }
+        if (rc) {
+            cudaFreeAsync(acc_heavy, st);
+            cudaFreeAsync(hcnt, st);
+            return rc;
+        }
+    }
     k_eloc_spin<<<g, 256, 0, st>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc, (unsigned long long *)stats,
-                                   pairs, phase_mask);
+                                   pairs, phase_mask, acc_heavy, t->thr_rowheavy);
+    if (acc_heavy) cudaFreeAsync(acc_heavy, st);
+    if (hcnt) cudaFreeAsync(hcnt, st);
+    if (hkeys) cudaFreeAsync(hkeys, st);
     return cuda_check(cudaGetLastError(), "structured local energy launch");
 }
