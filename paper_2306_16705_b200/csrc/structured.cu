@@ -294,7 +294,7 @@ __device__ __noinline__ void flush_queue(const GroupView &G, const TabSpin &T, i
 #define SCAN_LIMIT 8192
 #define WARPS_PER_BLOCK 8
 #ifndef NNQS_SPIN_MINB
-#define NNQS_SPIN_MINB 3
+#define NNQS_SPIN_MINB 4
 #endif
 #define QCAP 64
 
@@ -303,13 +303,19 @@ __device__ __noinline__ void flush_queue(const GroupView &G, const TabSpin &T, i
 // string lists; hits (group k, table index) go to a per-warp queue and are
 // evaluated 32 at a time, one per lane (slot s -> lane s mod 32, so the
 // summation order of a row is fixed by the row and the table).
+// PH selects the phases compiled into this instantiation: 1 diagonal, 2/4 same-
+// spin lists, 8 alpha x beta.  PH = 7 writes the row's partial sum to
+// `partial`; PH = 8 starts from it and finalises E_loc (two smaller kernels:
+// fewer registers, more resident warps, less instruction-cache pressure).
+template <int PH>
 __global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, GroupView G, TabSpin T, int64_t row_begin,
                                                    int64_t n_rows, double2 *out,
                                                    unsigned long long *stats, unsigned long long pairs,
-                                                   int phase_mask, const double2 *acc_heavy, int32_t thr_rowheavy) {
+                                                   int phase_mask, const double2 *acc_heavy, int32_t thr_rowheavy,
+                                                   double2 *partial) {
     __shared__ int2 s_q[WARPS_PER_BLOCK][QCAP];
     __shared__ uint8_t s_orb[WARPS_PER_BLOCK][4][64];   // occ(a), vir(a), occ(b), vir(b) of the row
-    if (stats && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(stats, pairs);
+    if ((PH & 8) && stats && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(stats, pairs);
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     int2 *q = s_q[threadIdx.x >> 5];
@@ -326,13 +332,18 @@ __global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, G
         const u64 x0 = xk.x, x1 = xk.y;
         const double2 lx = T.logpsi[i];
         if (!(lx.x > -INFINITY)) {
-            if (lane == 0) out[r] = make_double2(NAN, NAN);
+            if (lane == 0 && (PH & 8)) out[r] = make_double2(NAN, NAN);
             continue;
         }
         const double rel = lx.x - s;
         const bool direct = rel < -600.0;
         const u64 a = T.sa[i], b = T.sb[i];
         double ar = 0.0, ai = 0.0;
+        if (PH == 8 && lane == 0) {
+            const double2 pp = partial[r];
+            ar = pp.x;
+            ai = pp.y;
+        }
         __syncwarp();
         for (int j = lane; j < S.n; j += 32) {       // orbital lists (replace nth-set-bit searches)
             const u64 below = (1ULL << j) - 1;
@@ -369,7 +380,7 @@ __global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, G
             if (qn >= 32) flush(32);
         };
         // ---- diagonal group: warp-cooperative Pauli sum, fixed reduction
-        if (S.diag_k >= 0 && (phase_mask & 1)) {
+        if ((PH & 1) && S.diag_k >= 0 && (phase_mask & 1)) {
             const uint32_t gb = __ldg(G.goff + S.diag_k), ge = __ldg(G.goff + S.diag_k + 1);
             double hv = 0.0;
 #pragma unroll 4
@@ -386,7 +397,7 @@ __global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, G
         }
         // ---- (i) same beta string: x' = (a'', b), a'' in A(b);  (ii) same alpha string
         for (int ph = 0; ph < 2; ++ph) {
-            if (!(phase_mask & (2 << ph))) continue;
+            if (!(PH & (2 << ph)) || !(phase_mask & (2 << ph))) continue;
             const int32_t g = ph == 0 ? T.gb_of[i] : T.ga_of[i];
             const int32_t *off = ph == 0 ? T.offB : T.offA;
             const u64 *lst = ph == 0 ? T.listB_a : T.listA_b;
@@ -464,13 +475,13 @@ __global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, G
         }
         // ---- (iii) alpha single u x beta single v
         const int32_t ga_row = T.ga_of[i];
-        const bool row_heavy = acc_heavy && (T.offA[ga_row + 1] - T.offA[ga_row] > thr_rowheavy);
+        const bool row_heavy = (PH & 8) && acc_heavy && (T.offA[ga_row + 1] - T.offA[ga_row] > thr_rowheavy);
         if (row_heavy && lane == 0) {              // precomputed by the entry-driven join
             const double2 h = acc_heavy[r];
             ar += h.x;
             ai += h.y;
         }
-        if ((phase_mask & 8) && !row_heavy) {
+        if ((PH & 8) && (phase_mask & 8) && !row_heavy) {
             const u64 va = ~a & nmask, vb = ~b & nmask;
             const int noa = __popcll(a), nva = __popcll(va);
             const int nob = __popcll(b), nvb = __popcll(vb);
@@ -588,7 +599,8 @@ __global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, G
             ar += __shfl_xor_sync(0xffffffffu, ar, o);
             ai += __shfl_xor_sync(0xffffffffu, ai, o);
         }
-        if (lane == 0) {
+        if (lane == 0 && !(PH & 8)) partial[r] = make_double2(ar, ai);
+        if (lane == 0 && (PH & 8)) {
             double2 e;
             if (direct) {
                 e = make_double2(ar, ai);
@@ -1266,8 +1278,17 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
             return rc;
         }
     }
-    k_eloc_spin<<<g, 256, 0, st>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc, (unsigned long long *)stats,
-                                   pairs, phase_mask, acc_heavy, t->thr_rowheavy);
+    double2 *partial = nullptr;
+    rc = cuda_check(cudaMallocAsync((void **)&partial, 16 * n_rows + 16, st), "alloc partial");
+    if (!rc) {
+        k_eloc_spin<7><<<g, 256, 0, st>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc,
+                                          (unsigned long long *)stats, pairs, phase_mask, acc_heavy,
+                                          t->thr_rowheavy, partial);
+        k_eloc_spin<8><<<g, 256, 0, st>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc,
+                                          (unsigned long long *)stats, pairs, phase_mask, acc_heavy,
+                                          t->thr_rowheavy, partial);
+        cudaFreeAsync(partial, st);
+    }
     if (acc_heavy) cudaFreeAsync(acc_heavy, st);
     if (hcnt) cudaFreeAsync(hcnt, st);
     if (hkeys) cudaFreeAsync(hkeys, st);
