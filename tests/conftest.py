@@ -11,3 +11,7 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running CPU test")
+    # compile libnnqs.so (nvcc cross-compiles without a GPU) before any test module
+    # imports the package; the package itself refuses to import without it
+    import __graft_entry__
+    __graft_entry__.build()
