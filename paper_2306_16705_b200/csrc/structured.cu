@@ -146,6 +146,29 @@ __device__ __forceinline__ double group_value1(const GroupView &G, int32_t k, u6
     return hv;
 }
 
+// Warp-cooperative Pauli sum of strings [b, e): lane l takes b+l, b+l+32, ...
+// in ascending order (4 loads in flight), then a fixed butterfly.  Every lane
+// returns the group value.
+__device__ __forceinline__ double warp_strided_sum(const GroupView &G, uint32_t b, uint32_t e, u64 x0, u64 x1) {
+    const int lane = threadIdx.x & 31;
+    double hv = 0.0;
+    for (uint32_t t0 = b + lane; t0 < e; t0 += 128) {
+        ulonglong2 Z[4];
+        double d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const bool ok = t0 + 32 * u < e;
+            Z[u] = ok ? __ldg(G.tz + t0 + 32 * u) : make_ulonglong2(0, 0);
+            d[u] = ok ? __ldg(G.td + t0 + 32 * u) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (t0 + 32 * u < e) hv += flip_sign2(d[u], (__popcll(x0 & Z[u].x) + __popcll(x1 & Z[u].y)) & 1);
+    }
+    for (int o = 16; o; o >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, o);
+    return hv;
+}
+
 // spread the bits of a (alpha, spin 0) / b (beta, spin 1) onto qubits 2p+s
 __device__ __forceinline__ void spread_bit(int p, int s, u64 &w0, u64 &w1) {
     const int j = 2 * p + s;
@@ -240,17 +263,17 @@ __device__ __noinline__ void flush_queue(const GroupView &G, const TabSpin &T, i
     __syncwarp();
     int2 e = make_int2(-1, 0);
     uint32_t gb0 = 0, ge0 = 0;
+    double2 ps0 = make_double2(0.0, 0.0);
     if (lane < cnt) {
         e = q[lane];
         gb0 = __ldg(G.goff + e.x);
         ge0 = __ldg(G.goff + e.x + 1);
+        if (!direct) ps0 = __ldg(T.psi_hat + e.y);   // issued with the offsets, used after the sum
         ++c_hit;
     }
     auto add = [&](double hv, int64_t idx) {
-        double2 ps;
-        if (!direct) {
-            ps = __ldg(T.psi_hat + idx);
-        } else {
+        double2 ps = ps0;
+        if (direct) {
             const double2 l = T.logpsi[idx];
             const double m = exp(l.x - lx.x);
             double sn, cs;
@@ -262,10 +285,20 @@ __device__ __noinline__ void flush_queue(const GroupView &G, const TabSpin &T, i
     };
     const bool big = lane < cnt && ge0 - gb0 > 32;
     if (lane < cnt && !big) {
+        // 4 strings in flight per lane (loads issued before the sums; same order)
         double hv = 0.0;
-        for (uint32_t i = gb0; i < ge0; ++i) {
-            const ulonglong2 Z = __ldg(G.tz + i);
-            hv += flip_sign2(__ldg(G.td + i), (__popcll(x0 & Z.x) + __popcll(x1 & Z.y)) & 1);
+        for (uint32_t i0 = gb0; i0 < ge0; i0 += 4) {
+            ulonglong2 Z[4];
+            double d[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool ok = i0 + u < ge0;
+                Z[u] = ok ? __ldg(G.tz + i0 + u) : make_ulonglong2(0, 0);
+                d[u] = ok ? __ldg(G.td + i0 + u) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i0 + u < ge0) hv += flip_sign2(d[u], (__popcll(x0 & Z[u].x) + __popcll(x1 & Z[u].y)) & 1);
         }
         c_str += ge0 - gb0;
         add(hv, e.y);
@@ -275,12 +308,7 @@ __device__ __noinline__ void flush_queue(const GroupView &G, const TabSpin &T, i
         const int src = __ffs(bigs) - 1;
         bigs &= bigs - 1;
         const uint32_t b1 = __shfl_sync(0xffffffffu, gb0, src), e1 = __shfl_sync(0xffffffffu, ge0, src);
-        double hv = 0.0;
-        for (uint32_t t = b1 + lane; t < e1; t += 32) {
-            const ulonglong2 Z = __ldg(G.tz + t);
-            hv += flip_sign2(__ldg(G.td + t), (__popcll(x0 & Z.x) + __popcll(x1 & Z.y)) & 1);
-        }
-        for (int o = 16; o; o >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, o);
+        double hv = warp_strided_sum(G, b1, e1, x0, x1);
         if (lane == src) {
             add(hv, e.y);
             c_str += e1 - b1;
@@ -297,6 +325,7 @@ __device__ __noinline__ void flush_queue(const GroupView &G, const TabSpin &T, i
 #define NNQS_SPIN_MINB 4
 #endif
 #define QCAP 64
+#define HCAP 96
 
 // one warp per row; rows are table entries [row_begin, row_begin + n_rows).
 // Candidate x' are found by warp-uniform, 4-way unrolled scans of the table's
@@ -307,14 +336,15 @@ __device__ __noinline__ void flush_queue(const GroupView &G, const TabSpin &T, i
 // spin lists, 8 alpha x beta.  PH = 7 writes the row's partial sum to
 // `partial`; PH = 8 starts from it and finalises E_loc (two smaller kernels:
 // fewer registers, more resident warps, less instruction-cache pressure).
-template <int PH>
-__global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, GroupView G, TabSpin T, int64_t row_begin,
+template <int PH, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G, TabSpin T, int64_t row_begin,
                                                    int64_t n_rows, double2 *out,
                                                    unsigned long long *stats, unsigned long long pairs,
                                                    int phase_mask, const double2 *acc_heavy, int32_t thr_rowheavy,
                                                    double2 *partial) {
     __shared__ int2 s_q[WARPS_PER_BLOCK][QCAP];
     __shared__ uint8_t s_orb[WARPS_PER_BLOCK][4][64];   // occ(a), vir(a), occ(b), vir(b) of the row
+    __shared__ int2 s_h[(PH & 8) ? WARPS_PER_BLOCK : 1][HCAP];   // heavy adjacent alpha groups (g, u rank)
     if ((PH & 8) && stats && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(stats, pairs);
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -379,16 +409,40 @@ __global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, G
             qn += __popc(m);
             if (qn >= 32) flush(32);
         };
+        // Every lane holds a multimap match range [mb, me) and a tag; all matches of
+        // the warp are evaluated 32 at a time in (lane, position) order -- parallel
+        // dependent loads instead of one matching lane at a time.
+        auto drain = [&](int32_t mb, int32_t me, int32_t tag, auto &&eval) {
+            const int32_t len = me - mb;
+            int32_t incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const int32_t excl = incl - len;
+            const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            for (int32_t f0 = 0; f0 < total; f0 += 32) {
+                const int32_t f = f0 + lane;
+                int lo = 0;
+#pragma unroll
+                for (int st = 16; st; st >>= 1) {
+                    const int c = lo + st;
+                    const int32_t ex = __shfl_sync(0xffffffffu, excl, c & 31);
+                    if (c < 32 && ex <= f) lo = c;
+                }
+                const int32_t smb = __shfl_sync(0xffffffffu, mb, lo);
+                const int32_t sex = __shfl_sync(0xffffffffu, excl, lo);
+                const int32_t stag = __shfl_sync(0xffffffffu, tag, lo);
+                int32_t k = -1, idx = 0;
+                if (f < total) eval(smb + (f - sex), stag, k, idx);
+                push(k, idx);
+            }
+        };
         // ---- diagonal group: warp-cooperative Pauli sum, fixed reduction
         if ((PH & 1) && S.diag_k >= 0 && (phase_mask & 1)) {
             const uint32_t gb = __ldg(G.goff + S.diag_k), ge = __ldg(G.goff + S.diag_k + 1);
-            double hv = 0.0;
-#pragma unroll 4
-            for (uint32_t t = gb + lane; t < ge; t += 32) {
-                const ulonglong2 Z = __ldg(G.tz + t);
-                hv += flip_sign2(__ldg(G.td + t), (__popcll(x0 & Z.x) + __popcll(x1 & Z.y)) & 1);
-            }
-            for (int o = 16; o; o >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, o);
+            const double hv = warp_strided_sum(G, gb, ge, x0, x1);
             if (lane == 0) {
                 add(hv, i);
                 c_str += ge - gb;
@@ -452,24 +506,11 @@ __global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, G
                     }
                     int32_t mb = 0, me = 0;
                     if (live) mm_find(T, key, meta, mb, me);
-                    unsigned ball = __ballot_sync(0xffffffffu, me > mb);
-                    while (ball) {                       // matches of each probing lane, warp-wide
-                        const int src = __ffs(ball) - 1;
-                        ball &= ball - 1;
-                        const int32_t sb0 = __shfl_sync(0xffffffffu, mb, src);
-                        const int32_t se0 = __shfl_sync(0xffffffffu, me, src);
-                        const int swant = __shfl_sync(0xffffffffu, want, src);
-                        for (int32_t m0 = sb0; m0 < se0; m0 += 32) {
-                            const int32_t mj = m0 + lane;
-                            int32_t k = -1, idx = 0;
-                            if (mj < se0) {
-                                idx = __ldg(T.mm_val + mj);
-                                const u64 d = mine ^ __ldg(T.mm_str + mj);
-                                if (__popcll(d) == swant) k = same_spin_group(S, ph, d, swant);
-                            }
-                            push(k, idx);
-                        }
-                    }
+                    drain(mb, me, want, [&](int32_t mj, int32_t swant, int32_t &k, int32_t &idx) {
+                        idx = __ldg(T.mm_val + mj);
+                        const u64 d = mine ^ __ldg(T.mm_str + mj);
+                        if (__popcll(d) == swant) k = same_spin_group(S, ph, d, swant);
+                    });
                 }
             }
         }
@@ -486,8 +527,37 @@ __global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, G
             const int noa = __popcll(a), nva = __popcll(va);
             const int nob = __popcll(b), nvb = __popcll(vb);
             const int combos = noa * nva;
-            (void)nob;
             (void)nvb;
+            int nheavy = 0;                          // warp-uniform
+            int2 *hl = s_h[(PH & 8) ? (threadIdx.x >> 5) : 0];
+            // heavy alpha groups a' = a ^ u: probe (a', b - e_r) for every occupied beta r,
+            // nheavy x nob probes spread over the lanes, matches drained warp-wide
+            auto probe_heavy = [&]() {
+                __syncwarp();
+                const int ntask = nheavy * nob;
+                for (int t0 = 0; t0 < ntask; t0 += 32) {
+                    const int t = t0 + lane;
+                    int32_t mb = 0, me = 0, ur = 0;
+                    if (t < ntask) {
+                        const int h = t / nob, rr = t - h * nob;
+                        const int2 hv = hl[h];
+                        ur = hv.y;
+                        mm_find(T, b ^ (1ULL << occB[rr]), mm_meta(0, hv.x), mb, me);
+                        ++c_cand;
+                    }
+                    drain(mb, me, ur, [&](int32_t mj, int32_t sur, int32_t &k, int32_t &idx) {
+                        idx = __ldg(T.mm_val + mj);
+                        const u64 d = b ^ __ldg(T.mm_str + mj);
+                        if (d) {
+                            const int r1 = __ffsll((long long)d) - 1;
+                            const int r2 = 63 - __clzll((long long)d);
+                            k = __ldg(S.ab_k + (int64_t)sur * S.P + pair_rank(r1, r2, S.n));
+                        }
+                    });
+                }
+                nheavy = 0;
+                __syncwarp();
+            };
             for (int c0 = 0; c0 < combos; c0 += 32) {
                 const int cidx = c0 + lane;
                 int p = 0, qo = 0;
@@ -548,51 +618,13 @@ __global__ void __launch_bounds__(256, NNQS_SPIN_MINB) k_eloc_spin(SpinView S, G
                         push(k, k >= 0 ? __ldg(T.listA_idx + jj[u]) : 0);
                     }
                 }
-                // heavy adjacent alpha strings: multimap probes, one at a time
-                unsigned ball = __ballot_sync(0xffffffffu, heavy && !(phase_mask & 32));
-                while (ball) {
-                    const int src = __ffs(ball) - 1;
-                    ball &= ball - 1;
-                    const int pp = __shfl_sync(0xffffffffu, p, src);
-                    const int qq = __shfl_sync(0xffffffffu, qo, src);
-                    const int32_t gg = __shfl_sync(0xffffffffu, g2, src);
-                    const int32_t *abk = S.ab_k + pair_rank(min(pp, qq), max(pp, qq), S.n) * S.P;
-                    {
-                        // heavy alpha group a': probe (a', b - e_r) deletions of b
-                        const int nob1 = __popcll(b);
-                        const uint32_t meta = mm_meta(0, gg);
-                        for (int t0 = 0; t0 < nob1; t0 += 32) {
-                            const int t = t0 + lane;
-                            int32_t mb = 0, me = 0;
-                            if (t < nob1) {
-                                mm_find(T, b ^ (1ULL << occB[t]), meta, mb, me);
-                                ++c_cand;
-                            }
-                            unsigned ball2 = __ballot_sync(0xffffffffu, me > mb);
-                            while (ball2) {
-                                const int src = __ffs(ball2) - 1;
-                                ball2 &= ball2 - 1;
-                                const int32_t sb0 = __shfl_sync(0xffffffffu, mb, src);
-                                const int32_t se0 = __shfl_sync(0xffffffffu, me, src);
-                                for (int32_t m0 = sb0; m0 < se0; m0 += 32) {
-                                    const int32_t mj = m0 + lane;
-                                    int32_t k = -1, idx = 0;
-                                    if (mj < se0) {
-                                        idx = __ldg(T.mm_val + mj);
-                                        const u64 d = b ^ __ldg(T.mm_str + mj);
-                                        if (d) {
-                                            const int r1 = __ffsll((long long)d) - 1;
-                                            const int r2 = 63 - __clzll((long long)d);
-                                            k = __ldg(abk + pair_rank(r1, r2, S.n));
-                                        }
-                                    }
-                                    push(k, idx);
-                                }
-                            }
-                        }
-                    }
-                }
+                // heavy adjacent alpha strings: deferred to the warp's heavy list
+                const unsigned hb = __ballot_sync(0xffffffffu, heavy && !(phase_mask & 32));
+                if (heavy && !(phase_mask & 32)) hl[nheavy + __popc(hb & lt_mask)] = make_int2(g2, urank);
+                nheavy += __popc(hb);
+                if (nheavy > HCAP - 32) probe_heavy();
             }
+            probe_heavy();
         }
         if (qn > 0) flush(qn);
         for (int o = 16; o; o >>= 1) {
@@ -1281,12 +1313,17 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
     double2 *partial = nullptr;
     rc = cuda_check(cudaMallocAsync((void **)&partial, 16 * n_rows + 16, st), "alloc partial");
     if (!rc) {
-        k_eloc_spin<7><<<g, 256, 0, st>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc,
-                                          (unsigned long long *)stats, pairs, phase_mask, acc_heavy,
-                                          t->thr_rowheavy, partial);
-        k_eloc_spin<8><<<g, 256, 0, st>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc,
-                                          (unsigned long long *)stats, pairs, phase_mask, acc_heavy,
-                                          t->thr_rowheavy, partial);
+        static int minb = -1;   // resident blocks/SM of the two instantiations (tuning only)
+        if (minb < 0) {
+            const char *e = std::getenv("NNQS_MINB");
+            minb = e ? std::atoi(e) : 43;
+        }
+        auto launch = [&](auto kern) {
+            kern<<<g, 256, 0, st>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc, (unsigned long long *)stats,
+                                    pairs, phase_mask, acc_heavy, t->thr_rowheavy, partial);
+        };
+        if (minb / 10 == 3) launch(k_eloc_spin<7, 3>); else launch(k_eloc_spin<7, 4>);
+        if (minb % 10 == 3) launch(k_eloc_spin<8, 3>); else launch(k_eloc_spin<8, 4>);
         cudaFreeAsync(partial, st);
     }
     if (acc_heavy) cudaFreeAsync(acc_heavy, st);
