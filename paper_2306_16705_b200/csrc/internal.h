@@ -110,11 +110,9 @@ struct nnqs_table_s {
     int32_t *ah_vals = nullptr;
     u64 ah_mask = 0;
     // deletion-key multimap for heavy string groups (see structured.cu)
-    void *mm = nullptr;                        // unique-key hash slots {u64 key, u32 meta, u32 run}
+    void *mm = nullptr;                        // unique-key hash slots, 32 B: {u64 key, u32 meta, u32 beg | u32 end, pad}
     u64 mm_mask = 0;
-    int32_t *mm_run = nullptr;                 // [n_runs+1] run starts into mm_val
-    int32_t *mm_val = nullptr;                 // entry indices sorted by (meta, key, entry)
-    u64 *mm_str = nullptr;                     // ... and the entry's varying string
+    void *mm_ent = nullptr;                    // [m] {u64 varying string, u64 entry index}, sorted by (meta, key, entry)
     void *mm_buf = nullptr;
     int32_t thr_single = 0, thr_double = 0;    // list-length thresholds
     int32_t thr_rowheavy = 0;                  // alpha groups with more rows: entry-driven phase (iii)

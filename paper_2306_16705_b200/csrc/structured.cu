@@ -103,8 +103,7 @@ struct TabSpin {
     u64 ah_mask;
     const ulonglong2 *mm;     // deletion multimap: unique (key, meta) -> run id (y = meta | run << 32)
     u64 mm_mask;
-    const int32_t *mm_run, *mm_val;
-    const u64 *mm_str;
+    const ulonglong2 *mm_ent;  // {varying string, entry index} per multimap entry
     int32_t thr_single, thr_double;
 };
 
@@ -227,17 +226,19 @@ __device__ __forceinline__ int32_t same_spin_group(const SpinView &S, int spin, 
     return __ldg((spin ? S.quad_k1 : S.quad_k0) + quad_rank(p1, p2, p3, p4));
 }
 
-// multimap lookup: [beg, end) into mm_val of the entries stored under (key, meta)
+// multimap lookup: [beg, end) into mm_ent of the entries stored under (key, meta).
+// A slot is 32 B (one sector): {key, meta | beg << 32}, {end, -}.
 __device__ __forceinline__ void mm_find(const TabSpin &T, u64 key, uint32_t meta, int32_t &beg, int32_t &end) {
     u64 pos = mm_hash(key, meta) & T.mm_mask;
     beg = end = 0;
     while (true) {
-        const ulonglong2 v = __ldg(T.mm + pos);
-        const uint32_t run = (uint32_t)(v.y >> 32);
-        if (run == MM_EMPTY) return;
-        if (v.x == key && (uint32_t)v.y == meta) {
-            beg = __ldg(T.mm_run + run);
-            end = __ldg(T.mm_run + run + 1);
+        const ulonglong2 v = __ldg(T.mm + 2 * pos);
+        const ulonglong2 w = __ldg(T.mm + 2 * pos + 1);
+        const uint32_t sm = (uint32_t)v.y;
+        if (sm == MM_EMPTY) return;
+        if (v.x == key && sm == meta) {
+            beg = (int32_t)(v.y >> 32);
+            end = (int32_t)w.x;
             return;
         }
         pos = (pos + 1) & T.mm_mask;
@@ -255,12 +256,32 @@ __device__ __forceinline__ void nth_pair(int c, int &i, int &j) {
 // Evaluate the first cnt queued hits (lane l takes slot l), add their
 // contributions H * psi(x') to the lane accumulators, and shift the queue.
 // Out of line: it is reached from every candidate site, and inlining it there
-// overflowed the instruction cache.
-__device__ __noinline__ void flush_queue(const GroupView &G, const TabSpin &T, int2 *q, int qn, int cnt, u64 x0,
-                                         u64 x1, double2 lx, bool direct, double &ar, double &ai,
-                                         unsigned long long &c_hit, unsigned long long &c_str) {
+// overflowed the instruction cache.  Everything is passed and returned by value
+// (views by value, accumulators in/out): a reference argument of a call that
+// is not inlined forces the referenced object -- e.g. a kernel-parameter
+// struct -- into local memory.
+// The row being evaluated by a warp, and its per-lane accumulators, live in
+// shared memory: they are touched only here and at the row's start and end,
+// which keeps the scanning loops' register footprint (and spills) down.
+struct RowState {
+    u64 x0, x1;
+    double2 lx;
+    int direct;
+    int pad;
+};
+
+// Inlined at every push site: the ratio psi(x')/psi(x) of the rare rows with
+// psi_hat(x) < e^-600 (exp / sincos, large code) is a separate instantiation
+// (DIRECT), so this stays small and no ABI call forces the kernel's live
+// registers to local memory.
+template <bool DIRECT>
+__device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *psi_hat, const double2 *logpsi,
+                                             int2 *q, int qn, int cnt, const RowState *rs, double2 *acc) {
     const int lane = threadIdx.x & 31;
+    uint32_t c_hit = 0, c_str = 0;
     __syncwarp();
+    const u64 x0 = rs->x0, x1 = rs->x1;
+    constexpr bool direct = DIRECT;
     int2 e = make_int2(-1, 0);
     uint32_t gb0 = 0, ge0 = 0;
     double2 ps0 = make_double2(0.0, 0.0);
@@ -268,20 +289,23 @@ __device__ __noinline__ void flush_queue(const GroupView &G, const TabSpin &T, i
         e = q[lane];
         gb0 = __ldg(G.goff + e.x);
         ge0 = __ldg(G.goff + e.x + 1);
-        if (!direct) ps0 = __ldg(T.psi_hat + e.y);   // issued with the offsets, used after the sum
+        if (!direct) ps0 = __ldg(psi_hat + e.y);   // issued with the offsets, used after the sum
         ++c_hit;
     }
     auto add = [&](double hv, int64_t idx) {
         double2 ps = ps0;
         if (direct) {
-            const double2 l = T.logpsi[idx];
+            const double2 lx = rs->lx;
+            const double2 l = logpsi[idx];
             const double m = exp(l.x - lx.x);
             double sn, cs;
             sincos(l.y - lx.y, &sn, &cs);
             ps = make_double2(m * cs, m * sn);
         }
-        ar = fma(hv, ps.x, ar);
-        ai = fma(hv, ps.y, ai);
+        double2 a = acc[lane];
+        a.x = fma(hv, ps.x, a.x);
+        a.y = fma(hv, ps.y, a.y);
+        acc[lane] = a;
     };
     const bool big = lane < cnt && ge0 - gb0 > 32;
     if (lane < cnt && !big) {
@@ -317,6 +341,7 @@ __device__ __noinline__ void flush_queue(const GroupView &G, const TabSpin &T, i
     __syncwarp();
     if (lane < qn - cnt) q[lane] = q[lane + cnt];
     __syncwarp();
+    return make_uint2(c_hit, c_str);
 }
 
 #define SCAN_LIMIT 8192
@@ -336,7 +361,7 @@ __device__ __noinline__ void flush_queue(const GroupView &G, const TabSpin &T, i
 // spin lists, 8 alpha x beta.  PH = 7 writes the row's partial sum to
 // `partial`; PH = 8 starts from it and finalises E_loc (two smaller kernels:
 // fewer registers, more resident warps, less instruction-cache pressure).
-template <int PH, int MINB>
+template <int PH, int MINB, bool DIRECT>
 __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G, TabSpin T, int64_t row_begin,
                                                    int64_t n_rows, double2 *out,
                                                    unsigned long long *stats, unsigned long long pairs,
@@ -345,7 +370,9 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
     __shared__ int2 s_q[WARPS_PER_BLOCK][QCAP];
     __shared__ uint8_t s_orb[WARPS_PER_BLOCK][4][64];   // occ(a), vir(a), occ(b), vir(b) of the row
     __shared__ int2 s_h[(PH & 8) ? WARPS_PER_BLOCK : 1][HCAP];   // heavy adjacent alpha groups (g, u rank)
-    if ((PH & 8) && stats && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(stats, pairs);
+    __shared__ RowState s_row[WARPS_PER_BLOCK];
+    __shared__ double2 s_acc[WARPS_PER_BLOCK][32];
+    if ((PH & 8) && !DIRECT && stats && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(stats, pairs);
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     int2 *q = s_q[threadIdx.x >> 5];
@@ -355,26 +382,27 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const double s = dkey_inv2(*T.shift_key);
     const u64 nmask = S.n >= 64 ? ~0ULL : ((1ULL << S.n) - 1);
-    unsigned long long c_cand = 0, c_hit = 0, c_str = 0;
+    RowState *rs = &s_row[threadIdx.x >> 5];
+    double2 *acc = s_acc[threadIdx.x >> 5];
+    uint32_t c_cand = 0, c_hit = 0, c_str = 0;
     for (int64_t r = warp; r < n_rows; r += nwarps) {
         const int64_t i = row_begin + r;
-        const ulonglong2 xk = T.keys[i];
-        const u64 x0 = xk.x, x1 = xk.y;
-        const double2 lx = T.logpsi[i];
-        if (!(lx.x > -INFINITY)) {
-            if (lane == 0 && (PH & 8)) out[r] = make_double2(NAN, NAN);
+        const double2 lx0 = T.logpsi[i];
+        if (!(lx0.x > -INFINITY)) {
+            if (lane == 0 && (PH & 8) && !DIRECT) out[r] = make_double2(NAN, NAN);
             continue;
         }
-        const double rel = lx.x - s;
-        const bool direct = rel < -600.0;
+        if (((lx0.x - s) < -600.0) != DIRECT) continue;   // the other instantiation's row
         const u64 a = T.sa[i], b = T.sb[i];
-        double ar = 0.0, ai = 0.0;
-        if (PH == 8 && lane == 0) {
-            const double2 pp = partial[r];
-            ar = pp.x;
-            ai = pp.y;
-        }
         __syncwarp();
+        if (lane == 0) {
+            const ulonglong2 xk = T.keys[i];
+            rs->x0 = xk.x;
+            rs->x1 = xk.y;
+            rs->lx = lx0;
+            rs->direct = DIRECT;
+        }
+        acc[lane] = (PH == 8 && lane == 0) ? partial[r] : make_double2(0.0, 0.0);
         for (int j = lane; j < S.n; j += 32) {       // orbital lists (replace nth-set-bit searches)
             const u64 below = (1ULL << j) - 1;
             if ((a >> j) & 1) occA[__popcll(a & below)] = (uint8_t)j;
@@ -383,24 +411,11 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             else virB[j - __popcll(b & below)] = (uint8_t)j;
         }
         __syncwarp();
-        // contribution of one hit: H * psi(x') (psi_hat scale; divided by psi_hat(x) at the end)
-        auto add = [&](double hv, int64_t idx) {
-            double2 ps;
-            if (!direct) {
-                ps = __ldg(T.psi_hat + idx);
-            } else {
-                const double2 l = T.logpsi[idx];
-                const double m = exp(l.x - lx.x);
-                double sn, cs;
-                sincos(l.y - lx.y, &sn, &cs);
-                ps = make_double2(m * cs, m * sn);
-            }
-            ar = fma(hv, ps.x, ar);
-            ai = fma(hv, ps.y, ai);
-        };
         int qn = 0;                                  // warp-uniform queue length
         auto flush = [&](int cnt) {                  // lanes < cnt evaluate q[lane]
-            flush_queue(G, T, q, qn, cnt, x0, x1, lx, direct, ar, ai, c_hit, c_str);
+            const uint2 fo = flush_queue<DIRECT>(G, T.psi_hat, T.logpsi, q, qn, cnt, rs, acc);
+            c_hit += fo.x;
+            c_str += fo.y;
             qn -= cnt;
         };
         auto push = [&](int32_t k, int32_t idx) {    // all lanes; k < 0 = no hit
@@ -442,9 +457,14 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
         // ---- diagonal group: warp-cooperative Pauli sum, fixed reduction
         if ((PH & 1) && S.diag_k >= 0 && (phase_mask & 1)) {
             const uint32_t gb = __ldg(G.goff + S.diag_k), ge = __ldg(G.goff + S.diag_k + 1);
-            const double hv = warp_strided_sum(G, gb, ge, x0, x1);
-            if (lane == 0) {
-                add(hv, i);
+            const double hv = warp_strided_sum(G, gb, ge, rs->x0, rs->x1);
+            if (lane == 0) {   // x' = x: psi_hat(x) (or 1 on the direct path)
+                double2 ps = make_double2(1.0, 0.0);
+                if (!DIRECT) ps = __ldg(T.psi_hat + i);
+                double2 ac = acc[0];
+                ac.x = fma(hv, ps.x, ac.x);
+                ac.y = fma(hv, ps.y, ac.y);
+                acc[0] = ac;
                 c_str += ge - gb;
                 ++c_hit;
             }
@@ -462,10 +482,12 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             if (je - jb <= T.thr_double) {
                 for (int32_t j0 = jb; j0 < je; j0 += 128) {
                     u64 v[4];
+                    int32_t ix[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const int32_t j = j0 + 32 * u + lane;
                         v[u] = j < je ? __ldg(lst + j) : mine;
+                        ix[u] = j < je ? __ldg(lidx + j) : 0;
                     }
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
@@ -475,7 +497,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         int32_t k = -1;
                         if ((c == 2 || c == 4) && 2 * __popcll(mine & d) == c) k = same_spin_group(S, ph, d, c);
                         c_cand += j < je;
-                        push(k, k >= 0 ? __ldg(lidx + j) : 0);
+                        push(k, ix[u]);
                     }
                 }
             } else {
@@ -507,8 +529,9 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                     int32_t mb = 0, me = 0;
                     if (live) mm_find(T, key, meta, mb, me);
                     drain(mb, me, want, [&](int32_t mj, int32_t swant, int32_t &k, int32_t &idx) {
-                        idx = __ldg(T.mm_val + mj);
-                        const u64 d = mine ^ __ldg(T.mm_str + mj);
+                        const ulonglong2 en = __ldg(T.mm_ent + mj);
+                        idx = (int32_t)en.y;
+                        const u64 d = mine ^ en.x;
                         if (__popcll(d) == swant) k = same_spin_group(S, ph, d, swant);
                     });
                 }
@@ -519,8 +542,10 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
         const bool row_heavy = (PH & 8) && acc_heavy && (T.offA[ga_row + 1] - T.offA[ga_row] > thr_rowheavy);
         if (row_heavy && lane == 0) {              // precomputed by the entry-driven join
             const double2 h = acc_heavy[r];
-            ar += h.x;
-            ai += h.y;
+            double2 ac = acc[0];
+            ac.x += h.x;
+            ac.y += h.y;
+            acc[0] = ac;
         }
         if ((PH & 8) && (phase_mask & 8) && !row_heavy) {
             const u64 va = ~a & nmask, vb = ~b & nmask;
@@ -546,8 +571,9 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         ++c_cand;
                     }
                     drain(mb, me, ur, [&](int32_t mj, int32_t sur, int32_t &k, int32_t &idx) {
-                        idx = __ldg(T.mm_val + mj);
-                        const u64 d = b ^ __ldg(T.mm_str + mj);
+                        const ulonglong2 en = __ldg(T.mm_ent + mj);
+                        idx = (int32_t)en.y;
+                        const u64 d = b ^ en.x;
                         if (d) {
                             const int r1 = __ffsll((long long)d) - 1;
                             const int r2 = 63 - __clzll((long long)d);
@@ -588,7 +614,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                 // flattened scan of all light lists of this chunk: 128 entries per warp step
                 for (int32_t f0 = 0; f0 < ((phase_mask & 16) ? 0 : total); f0 += 128) {
                     u64 v[4];
-                    int32_t jj[4], ur[4];
+                    int32_t jj[4], ur[4], ix[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const int32_t f = f0 + 32 * u + lane;
@@ -604,6 +630,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         ur[u] = __shfl_sync(0xffffffffu, urank, lo);
                         jj[u] = ob + (f - oe);
                         v[u] = f < total ? __ldg(T.listA_b + jj[u]) : b;
+                        ix[u] = f < total ? __ldg(T.listA_idx + jj[u]) : 0;   // issued with v: no dependent load on a hit
                     }
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
@@ -615,7 +642,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                             k = __ldg(S.ab_k + (int64_t)ur[u] * S.P + pair_rank(r1, r2, S.n));
                         }
                         c_cand += (f0 + 32 * u + lane) < total;
-                        push(k, k >= 0 ? __ldg(T.listA_idx + jj[u]) : 0);
+                        push(k, ix[u]);
                     }
                 }
                 // heavy adjacent alpha strings: deferred to the warp's heavy list
@@ -627,6 +654,11 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             probe_heavy();
         }
         if (qn > 0) flush(qn);
+        __syncwarp();
+        double ar = acc[lane].x, ai = acc[lane].y;
+        const double2 lx = rs->lx;
+        constexpr bool direct = DIRECT;
+        const double rel = lx.x - s;
         for (int o = 16; o; o >>= 1) {
             ar += __shfl_xor_sync(0xffffffffu, ar, o);
             ai += __shfl_xor_sync(0xffffffffu, ai, o);
@@ -653,9 +685,9 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             c_str += __shfl_xor_sync(0xffffffffu, c_str, o);
         }
         if (lane == 0) {
-            atomicAdd((unsigned long long *)stats + 1, c_cand);
-            atomicAdd((unsigned long long *)stats + 2, c_hit);
-            atomicAdd((unsigned long long *)stats + 3, c_str);
+            atomicAdd((unsigned long long *)stats + 1, (unsigned long long)c_cand);
+            atomicAdd((unsigned long long *)stats + 2, (unsigned long long)c_hit);
+            atomicAdd((unsigned long long *)stats + 3, (unsigned long long)c_str);
         }
     }
 }
@@ -789,27 +821,35 @@ __global__ void k_mm_heads(const u64 *K2, const uint32_t *M2, int64_t m, int32_t
 }
 
 __global__ void k_mm_runs(const u64 *K2, const uint32_t *M2, const int32_t *P2, const int32_t *V, const u64 *SV,
-                          const int32_t *rid, int64_t m, int32_t *run_start, int32_t *val, u64 *str,
-                          ulonglong2 *slots, u64 mask) {
+                          const int32_t *rid, int64_t m, int32_t *run_start, ulonglong2 *ent) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
          j += (int64_t)gridDim.x * blockDim.x) {
-        val[j] = V[P2[j]];
-        str[j] = SV[P2[j]];
+        ent[j] = make_ulonglong2(SV[P2[j]], (u64)(uint32_t)V[P2[j]]);
         const int32_t r = rid[j] - 1;
-        if (j == 0 || K2[j] != K2[j - 1] || M2[j] != M2[j - 1]) {
-            run_start[r] = (int32_t)j;
-            u64 s = mm_hash(K2[j], M2[j]) & mask;
-            while (true) {
-                uint32_t *w = reinterpret_cast<uint32_t *>(slots + s);
-                if (atomicCAS(w + 3, MM_EMPTY, (uint32_t)r) == MM_EMPTY) {
-                    slots[s].x = K2[j];
-                    w[2] = M2[j];
-                    break;
-                }
-                s = (s + 1) & mask;
-            }
-        }
+        if (j == 0 || K2[j] != K2[j - 1] || M2[j] != M2[j - 1]) run_start[r] = (int32_t)j;
         if (j == m - 1) run_start[r + 1] = (int32_t)m;
+    }
+}
+
+// one slot per run: claimed by CAS on the meta word, then key and bounds written
+__global__ void k_mm_slots(const u64 *K2, const uint32_t *M2, const int32_t *run_start, int64_t nruns,
+                           ulonglong2 *slots, u64 mask) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nruns;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t j = run_start[r], je = run_start[r + 1];
+        const u64 key = K2[j];
+        const uint32_t meta = M2[j];
+        u64 s = mm_hash(key, meta) & mask;
+        while (true) {
+            uint32_t *w = reinterpret_cast<uint32_t *>(slots + 2 * s);
+            if (atomicCAS(w + 2, MM_EMPTY, meta) == MM_EMPTY) {
+                slots[2 * s].x = key;
+                w[3] = (uint32_t)j;
+                slots[2 * s + 1] = make_ulonglong2((u64)(uint32_t)je, 0);
+                break;
+            }
+            s = (s + 1) & mask;
+        }
     }
 }
 
@@ -848,9 +888,10 @@ __global__ void __launch_bounds__(256) k_hj_emit(SpinView S, TabSpin T, const in
             mm_find(T, b2 ^ (m1 & (~m1 + 1)), meta, mb, me);
             ++probes;
             for (int32_t mj = mb; mj < me; ++mj) {
-                const int32_t e = T.mm_val[mj];
+                const ulonglong2 en = T.mm_ent[mj];
+                const int32_t e = (int32_t)en.y;
                 if (e < row_begin || e >= row_end) continue;
-                const u64 d = T.mm_str[mj] ^ b2;
+                const u64 d = en.x ^ b2;
                 if (!d) continue;
                 const int r1 = __ffsll((long long)d) - 1, r2 = 63 - __clzll((long long)d);
                 if (abk[pair_rank(r1, r2, S.n)] < 0) continue;
@@ -1054,10 +1095,8 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
             if (rc) return rc;
             t->mm = t->mm_buf;
             t->mm_mask = 0;
-            t->mm_run = (int32_t *)((char *)t->mm_buf + 16);
-            t->mm_val = (int32_t *)((char *)t->mm_buf + 32);
-            t->mm_str = (u64 *)((char *)t->mm_buf + 48);
-            cudaMemsetAsync(t->mm, 0xFF, 16, st);
+            t->mm_ent = (char *)t->mm_buf + 64;
+            cudaMemsetAsync(t->mm, 0xFF, 32, st);
         }
         return rc;
     }
@@ -1079,7 +1118,7 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
     auto take = [&](size_t b) { char *p = sp; sp += r16(b); return p; };
     u64 *K = (u64 *)take(8 * m), *K1 = (u64 *)take(8 * m), *K2 = (u64 *)take(8 * m), *SV = (u64 *)take(8 * m);
     uint32_t *M = (uint32_t *)take(4 * m), *M1 = (uint32_t *)take(4 * m), *M2 = (uint32_t *)take(4 * m);
-    int32_t *V = (int32_t *)take(4 * m), *io = (int32_t *)take(4 * m), *P1 = (int32_t *)take(4 * m),
+    int32_t *V = (int32_t *)take(4 * m), *io = (int32_t *)take(4 * (m + 1)), *P1 = (int32_t *)take(4 * m),
             *P2 = (int32_t *)take(4 * m);
     void *ct = take(ctb);
     const int gm = grid_for(m, 256);
@@ -1101,18 +1140,17 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
     if (rc) { cudaFreeAsync(sc, st); cudaFreeAsync(eoff, st); return rc; }
     u64 slots = 2;
     while (slots < 2 * (u64)nruns) slots <<= 1;
-    const size_t pbytes = r16(16 * slots) + r16(4 * ((size_t)nruns + 1)) + r16(4 * m) + r16(8 * m);
+    const size_t pbytes = r16(32 * slots) + r16(16 * m);
     rc = cuda_check(cudaMallocAsync(&t->mm_buf, pbytes, st), "alloc multimap");
     if (rc) { cudaFreeAsync(sc, st); cudaFreeAsync(eoff, st); return rc; }
     t->mm = t->mm_buf;
     t->mm_mask = slots - 1;
-    t->mm_run = (int32_t *)((char *)t->mm_buf + r16(16 * slots));
-    t->mm_val = (int32_t *)((char *)t->mm_run + r16(4 * ((size_t)nruns + 1)));
-    t->mm_str = (u64 *)((char *)t->mm_val + r16(4 * m));
+    t->mm_ent = (char *)t->mm_buf + r16(32 * slots);
     t->bytes += (int64_t)pbytes;
-    cudaMemsetAsync(t->mm, 0xFF, 16 * slots, st);
-    k_mm_runs<<<gm, 256, 0, st>>>(K2, M2, P2, V, SV, P1, m, t->mm_run, t->mm_val, t->mm_str, (ulonglong2 *)t->mm,
-                                  t->mm_mask);
+    cudaMemsetAsync(t->mm, 0xFF, 32 * slots, st);
+    int32_t *run_start = io;   // head flags are dead after the scan; io holds m + 1 ints >= nruns + 1
+    k_mm_runs<<<gm, 256, 0, st>>>(K2, M2, P2, V, SV, P1, m, run_start, (ulonglong2 *)t->mm_ent);
+    k_mm_slots<<<grid_for(nruns, 256), 256, 0, st>>>(K2, M2, run_start, nruns, (ulonglong2 *)t->mm, t->mm_mask);
     cudaFreeAsync(sc, st);
     cudaFreeAsync(eoff, st);
     return cuda_check(cudaGetLastError(), "multimap kernels");
@@ -1247,7 +1285,7 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
     TabSpin tv{t->n, (const ulonglong2 *)t->keys, (const double2 *)t->logpsi, (const double2 *)t->psi_hat,
                t->slots, t->bucket_mask, t->shift_key, t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB,
                t->listA_b, t->listB_a, t->listA_idx, t->listB_idx, t->ah_keys, t->ah_vals, t->ah_mask,
-               (const ulonglong2 *)t->mm, t->mm_mask, t->mm_run, t->mm_val, t->mm_str, t->thr_single,
+               (const ulonglong2 *)t->mm, t->mm_mask, (const ulonglong2 *)t->mm_ent, t->thr_single,
                t->thr_double};
     const int64_t threads = n_rows * 32;
     int g = (int)std::min<int64_t>((threads + 255) / 256, 148 * 64);
@@ -1316,14 +1354,26 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
         static int minb = -1;   // resident blocks/SM of the two instantiations (tuning only)
         if (minb < 0) {
             const char *e = std::getenv("NNQS_MINB");
-            minb = e ? std::atoi(e) : 43;
+            minb = e ? std::atoi(e) : 33;
         }
         auto launch = [&](auto kern) {
             kern<<<g, 256, 0, st>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc, (unsigned long long *)stats,
                                     pairs, phase_mask, acc_heavy, t->thr_rowheavy, partial);
         };
-        if (minb / 10 == 3) launch(k_eloc_spin<7, 3>); else launch(k_eloc_spin<7, 4>);
-        if (minb % 10 == 3) launch(k_eloc_spin<8, 3>); else launch(k_eloc_spin<8, 4>);
+        switch (minb / 10) {
+            case 3: launch(k_eloc_spin<7, 3, false>); break;
+            case 5: launch(k_eloc_spin<7, 5, false>); break;
+            case 6: launch(k_eloc_spin<7, 6, false>); break;
+            default: launch(k_eloc_spin<7, 4, false>);
+        }
+        launch(k_eloc_spin<7, 4, true>);
+        switch (minb % 10) {
+            case 3: launch(k_eloc_spin<8, 3, false>); break;
+            case 5: launch(k_eloc_spin<8, 5, false>); break;
+            case 6: launch(k_eloc_spin<8, 6, false>); break;
+            default: launch(k_eloc_spin<8, 4, false>);
+        }
+        launch(k_eloc_spin<8, 4, true>);
         cudaFreeAsync(partial, st);
     }
     if (acc_heavy) cudaFreeAsync(acc_heavy, st);
