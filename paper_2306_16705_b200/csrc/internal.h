@@ -53,6 +53,13 @@ struct SpinIndex {
     std::vector<int32_t> pair_k[2];   // [P]   2-site groups per spin
     std::vector<int32_t> quad_k[2];   // [Q]   4-site same-spin groups
     std::vector<int32_t> ab_k;        // [P*P] alpha pair x beta pair groups
+    // In-sector folded Pauli table (same groups, CSR): for a hit x' = x ^ X with
+    // x and x' in one (N_alpha, N_beta) sector, (-1)^{popc(x & F)} is a known
+    // constant for F = the pair masks of X (-1 each) or a same-spin quad (+1),
+    // so the strings Z and Z ^ F of a group merge into one.
+    std::vector<uint32_t> foff;       // [K+1]
+    std::vector<u64> fz;              // [M][2]
+    std::vector<double> fd;           // [M]
 };
 int nnqs_spin_index_build(const HostTable &H, SpinIndex &S);
 struct nnqs_ham_s;
@@ -72,6 +79,9 @@ struct DeviceHam {
     int32_t *pair_k[2] = {nullptr, nullptr};
     int32_t *quad_k[2] = {nullptr, nullptr};
     int32_t *ab_k = nullptr;
+    uint32_t *foff = nullptr;  // folded table (structured path)
+    void *fz = nullptr;
+    double *fd = nullptr;
     int64_t bytes = 0;
 };
 

@@ -168,13 +168,6 @@ __device__ __forceinline__ double warp_strided_sum(const GroupView &G, uint32_t 
     return hv;
 }
 
-// spread the bits of a (alpha, spin 0) / b (beta, spin 1) onto qubits 2p+s
-__device__ __forceinline__ void spread_bit(int p, int s, u64 &w0, u64 &w1) {
-    const int j = 2 * p + s;
-    if (j < 64) w0 ^= 1ULL << j;
-    else w1 ^= 1ULL << (j - 64);
-}
-
 __device__ __forceinline__ int32_t alpha_lookup(const TabSpin &T, u64 a) {
     u64 s = mix64(a) & T.ah_mask;
     while (true) {
@@ -182,26 +175,6 @@ __device__ __forceinline__ int32_t alpha_lookup(const TabSpin &T, u64 a) {
         if (v < 0) return -1;
         if (__ldg(T.ah_keys + s) == a) return v;
         s = (s + 1) & T.ah_mask;
-    }
-}
-
-__device__ __forceinline__ int64_t probe_key(const TabSpin &T, u64 h, u64 p0, u64 p1) {
-    u64 b = h & T.bucket_mask;
-    const uint32_t fp = (uint32_t)(h >> 32);
-    while (true) {
-        const ulonglong2 *bk = reinterpret_cast<const ulonglong2 *>(T.slots + 4 * b);
-        const ulonglong2 s01 = __ldg(bk), s23 = __ldg(bk + 1);
-        const u64 s[4] = {s01.x, s01.y, s23.x, s23.y};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            if (s[i] == 0xFFFFFFFFFFFFFFFFULL) return -1;
-            if ((uint32_t)(s[i] >> 32) == fp) {
-                const uint32_t r = (uint32_t)s[i];
-                const ulonglong2 k = __ldg(T.keys + r);
-                if (k.x == p0 && k.y == p1) return (int64_t)r;
-            }
-        }
-        b = (b + 1) & T.bucket_mask;
     }
 }
 
@@ -476,7 +449,6 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             const int32_t *off = ph == 0 ? T.offB : T.offA;
             const u64 *lst = ph == 0 ? T.listB_a : T.listA_b;
             const int32_t *lidx = ph == 0 ? T.listB_idx : T.listA_idx;
-            const u64 *str = ph == 0 ? T.sa : T.sb;          // the varying string of an entry
             const u64 mine = ph == 0 ? a : b;
             const int32_t jb = off[g], je = off[g + 1];
             if (je - jb <= T.thr_double) {
@@ -1028,6 +1000,55 @@ int nnqs_spin_index_build(const HostTable &H, SpinIndex &S) {
             S.ab_k[pair_rank(pos[0][0], pos[0][1], n) * S.P + pair_rank(pos[1][0], pos[1][1], n)] = (int32_t)k;
         else return NNQS_OK;               // not a single/double excitation pattern
     }
+    // ---- in-sector folding (see SpinIndex): generators F of each group type
+    S.foff.assign(K + 1, 0);
+    S.fz.clear();
+    S.fd.clear();
+    for (int64_t k = 0; k < K; ++k) {
+        u64 X[2] = {H.x[2 * k], H.x[2 * k + 1]};
+        u64 F[2][2] = {{0, 0}, {0, 0}};
+        int nf = 0;
+        u64 xs[2][2] = {{0, 0}, {0, 0}};        // X restricted to spin s (qubits 2p+s)
+        for (int w = 0; w < 2; ++w) {
+            xs[0][w] = X[w] & 0x5555555555555555ULL;
+            xs[1][w] = X[w] & 0xAAAAAAAAAAAAAAAAULL;
+        }
+        const int ca = __builtin_popcountll(xs[0][0]) + __builtin_popcountll(xs[0][1]);
+        const int cb = __builtin_popcountll(xs[1][0]) + __builtin_popcountll(xs[1][1]);
+        if (ca == 2 || ca == 4) { F[nf][0] = xs[0][0]; F[nf][1] = xs[0][1]; ++nf; }   // sign (-1)^{ca/2}
+        if (cb == 2 || cb == 4) { F[nf][0] = xs[1][0]; F[nf][1] = xs[1][1]; ++nf; }
+        std::vector<std::pair<std::pair<u64, u64>, long double>> acc;
+        for (int64_t t = H.off[k]; t < H.off[k + 1]; ++t) {
+            u64 z0 = H.z[2 * t], z1 = H.z[2 * t + 1];
+            long double d = H.d[t];
+            // canonical representative: clear the lowest set bit of each generator
+            for (int g = 0; g < nf; ++g) {
+                const int cnt = __builtin_popcountll(F[g][0]) + __builtin_popcountll(F[g][1]);
+                const u64 lowbit0 = F[g][0] ? (F[g][0] & (~F[g][0] + 1)) : 0;
+                const u64 lowbit1 = F[g][0] ? 0 : (F[g][1] & (~F[g][1] + 1));
+                const bool has = (z0 & lowbit0) || (z1 & lowbit1);
+                if (has) {
+                    z0 ^= F[g][0];
+                    z1 ^= F[g][1];
+                    if (cnt == 2) d = -d;      // (-1)^{popc(x & F)} = -1 in sector (one of the pair set)
+                }                              // cnt == 4: +1 (two of the quad set)
+            }
+            acc.push_back({{z1, z0}, d});
+        }
+        std::sort(acc.begin(), acc.end(), [](const auto &a, const auto &b) { return a.first < b.first; });
+        for (size_t u = 0; u < acc.size();) {
+            size_t v = u;
+            long double sum = 0.0L;
+            while (v < acc.size() && acc[v].first == acc[u].first) sum += acc[v++].second;
+            if ((double)sum != 0.0) {
+                S.fz.push_back(acc[u].first.second);
+                S.fz.push_back(acc[u].first.first);
+                S.fd.push_back((double)sum);
+            }
+            u = v;
+        }
+        S.foff[k + 1] = (uint32_t)S.fd.size();
+    }
     S.ok = true;
     return NNQS_OK;
 }
@@ -1049,6 +1070,16 @@ int nnqs_spin_index_upload(nnqs_ham h) {
     if ((rc = cuda_check(cudaMalloc((void **)&D.ab_k, bab), "alloc ab_k"))) return rc;
     if ((rc = cuda_check(cudaMemcpy(D.ab_k, S.ab_k.data(), bab, cudaMemcpyHostToDevice), "copy ab_k"))) return rc;
     D.bytes += (int64_t)bab;
+    const size_t bo = 4 * S.foff.size(), bz = 8 * std::max<size_t>(S.fz.size(), 2), bd = 8 * std::max<size_t>(S.fd.size(), 1);
+    if ((rc = cuda_check(cudaMalloc((void **)&D.foff, bo), "alloc foff"))) return rc;
+    if ((rc = cuda_check(cudaMalloc((void **)&D.fz, bz), "alloc fz"))) return rc;
+    if ((rc = cuda_check(cudaMalloc((void **)&D.fd, bd), "alloc fd"))) return rc;
+    if ((rc = cuda_check(cudaMemcpy(D.foff, S.foff.data(), bo, cudaMemcpyHostToDevice), "copy foff"))) return rc;
+    if (!S.fd.empty()) {
+        if ((rc = cuda_check(cudaMemcpy(D.fz, S.fz.data(), 8 * S.fz.size(), cudaMemcpyHostToDevice), "copy fz"))) return rc;
+        if ((rc = cuda_check(cudaMemcpy(D.fd, S.fd.data(), 8 * S.fd.size(), cudaMemcpyHostToDevice), "copy fd"))) return rc;
+    }
+    D.bytes += (int64_t)(bo + bz + bd);
     return NNQS_OK;
 }
 
@@ -1061,6 +1092,12 @@ void nnqs_spin_index_release(nnqs_ham h) {
     }
     cudaFree(D.ab_k);
     D.ab_k = nullptr;
+    cudaFree(D.foff);
+    cudaFree(D.fz);
+    cudaFree(D.fd);
+    D.foff = nullptr;
+    D.fz = nullptr;
+    D.fd = nullptr;
 }
 
 namespace {
@@ -1281,7 +1318,7 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
     const SpinIndex &S = h->spin;
     const DeviceHam &D = h->dev;
     SpinView sv{S.n, S.P, D.pair_k[0], D.pair_k[1], D.quad_k[0], D.quad_k[1], D.ab_k, S.diag_k};
-    GroupView gv{D.goff, (const ulonglong2 *)D.tz, D.td};
+    GroupView gv{D.foff, (const ulonglong2 *)D.fz, D.fd};   // in-sector folded strings
     TabSpin tv{t->n, (const ulonglong2 *)t->keys, (const double2 *)t->logpsi, (const double2 *)t->psi_hat,
                t->slots, t->bucket_mask, t->shift_key, t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB,
                t->listA_b, t->listB_a, t->listA_idx, t->listB_idx, t->ah_keys, t->ah_vals, t->ah_mask,
@@ -1354,7 +1391,7 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
         static int minb = -1;   // resident blocks/SM of the two instantiations (tuning only)
         if (minb < 0) {
             const char *e = std::getenv("NNQS_MINB");
-            minb = e ? std::atoi(e) : 33;
+            minb = e ? std::atoi(e) : 44;
         }
         auto launch = [&](auto kern) {
             kern<<<g, 256, 0, st>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc, (unsigned long long *)stats,

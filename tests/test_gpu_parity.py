@@ -196,8 +196,10 @@ def test_c5_full_launch_sampled(nnqs, dev, c5):
 
 
 def test_c5_structured_equals_literal_hits(nnqs, dev, c5):
-    """On a 4096-row slice of C5: identical hit and string counts for the two
-    enumerations, and E_loc within tolerance of each other."""
+    """On a 4096-row slice of C5: identical hit counts for the two enumerations
+    (the same (row, group) pairs are found), E_loc within tolerance of each
+    other.  The structured path evaluates the in-sector folded strings (DESIGN.md
+    R21), so it evaluates fewer strings than the literal loop."""
     m, st, ham, tab = c5
     s1 = torch.zeros(4, dtype=torch.int64, device=dev)
     s2 = torch.zeros(4, dtype=torch.int64, device=dev)
@@ -208,7 +210,7 @@ def test_c5_structured_equals_literal_hits(nnqs, dev, c5):
     finally:
         nnqs.nnqs_set_algorithm(nnqs.ALGO_AUTO)
     s1, s2 = s1.cpu().numpy(), s2.cpu().numpy()
-    assert s1[2] == s2[2] and s1[3] == s2[3]
+    assert s1[2] == s2[2] and s1[3] < s2[3]
     assert np.max(np.abs(a - b) / np.maximum(np.abs(b), 1.0)) < 1e-9
 
 
@@ -335,7 +337,7 @@ def test_structured_equals_literal(nnqs, dev, c, variant):
     s1, s2 = s1.cpu().numpy(), s2.cpu().numpy()
     assert s1[0] == s2[0] == n * ham.info()["n_groups"]
     assert s1[2] == s2[2]                       # identical hit sets (counts)
-    assert s1[3] == s2[3]                       # identical Pauli strings evaluated
+    assert s1[3] <= s2[3]                       # in-sector folded strings (R21): never more
     ref, scale = R.eloc(m.h1, m.h2, m.e_core, st.keys, st.logpsi, keys=st.keys, logpsi=st.logpsi, with_scale=True)
     _assert_close(a, ref, scale, "structured")
     _assert_close(b, ref, scale, "literal")
