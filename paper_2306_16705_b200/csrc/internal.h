@@ -122,6 +122,8 @@ struct nnqs_table_s {
     // deletion-key multimap for heavy string groups (see structured.cu)
     void *mm = nullptr;                        // unique-key hash slots, 32 B: {u64 key, u32 meta, u32 beg | u32 end, pad}
     u64 mm_mask = 0;
+    u64 *mm_bloom = nullptr;                   // blocked Bloom filter over (key, meta): 2 bits in one word
+    u64 mm_bloom_mask = 0;                     // words - 1
     void *mm_ent = nullptr;                    // [m] {u64 varying string, u64 entry index}, sorted by (meta, key, entry)
     void *mm_buf = nullptr;
     int32_t thr_single = 0, thr_double = 0;    // list-length thresholds

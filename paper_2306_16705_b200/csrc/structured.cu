@@ -103,6 +103,8 @@ struct TabSpin {
     u64 ah_mask;
     const ulonglong2 *mm;     // deletion multimap: unique (key, meta) -> run id (y = meta | run << 32)
     u64 mm_mask;
+    const u64 *mm_bloom;      // ~8 bits per run: most probes miss (C5: ~80%) and stop here, in L2
+    u64 mm_bloom_mask;
     const ulonglong2 *mm_ent;  // {varying string, entry index} per multimap entry
     int32_t thr_single, thr_double;
 };
@@ -202,8 +204,11 @@ __device__ __forceinline__ int32_t same_spin_group(const SpinView &S, int spin, 
 // multimap lookup: [beg, end) into mm_ent of the entries stored under (key, meta).
 // A slot is 32 B (one sector): {key, meta | beg << 32}, {end, -}.
 __device__ __forceinline__ void mm_find(const TabSpin &T, u64 key, uint32_t meta, int32_t &beg, int32_t &end) {
-    u64 pos = mm_hash(key, meta) & T.mm_mask;
+    const u64 h = mm_hash(key, meta);
     beg = end = 0;
+    const u64 bw = __ldg(T.mm_bloom + ((h >> 32) & T.mm_bloom_mask));
+    if (!((bw >> ((h >> 20) & 63)) & (bw >> ((h >> 26) & 63)) & 1)) return;
+    u64 pos = h & T.mm_mask;
     while (true) {
         const ulonglong2 v = __ldg(T.mm + 2 * pos);
         const ulonglong2 w = __ldg(T.mm + 2 * pos + 1);
@@ -339,7 +344,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                                                    int64_t n_rows, double2 *out,
                                                    unsigned long long *stats, unsigned long long pairs,
                                                    int phase_mask, const double2 *acc_heavy, int32_t thr_rowheavy,
-                                                   double2 *partial) {
+                                                   double2 *partial, unsigned long long *row_ctr) {
     __shared__ int2 s_q[WARPS_PER_BLOCK][QCAP];
     __shared__ uint8_t s_orb[WARPS_PER_BLOCK][4][64];   // occ(a), vir(a), occ(b), vir(b) of the row
     __shared__ int2 s_h[(PH & 8) ? WARPS_PER_BLOCK : 1][HCAP];   // heavy adjacent alpha groups (g, u rank)
@@ -358,7 +363,15 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
     RowState *rs = &s_row[threadIdx.x >> 5];
     double2 *acc = s_acc[threadIdx.x >> 5];
     uint32_t c_cand = 0, c_hit = 0, c_str = 0;
-    for (int64_t r = warp; r < n_rows; r += nwarps) {
+    // rows: grid-stride, or (row_ctr != nullptr) handed out one at a time from a
+    // global counter, so a few expensive rows do not leave other warps idle
+    auto next_row = [&](int64_t cur) -> int64_t {
+        if (!row_ctr) return cur + nwarps;
+        unsigned long long v = 0;
+        if (lane == 0) v = atomicAdd(row_ctr, 1ULL);
+        return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+    };
+    for (int64_t r = row_ctr ? next_row(0) : warp; r < n_rows; r = next_row(r)) {
         const int64_t i = row_begin + r;
         const double2 lx0 = T.logpsi[i];
         if (!(lx0.x > -INFINITY)) {
@@ -805,13 +818,15 @@ __global__ void k_mm_runs(const u64 *K2, const uint32_t *M2, const int32_t *P2, 
 
 // one slot per run: claimed by CAS on the meta word, then key and bounds written
 __global__ void k_mm_slots(const u64 *K2, const uint32_t *M2, const int32_t *run_start, int64_t nruns,
-                           ulonglong2 *slots, u64 mask) {
+                           ulonglong2 *slots, u64 mask, u64 *bloom, u64 bmask) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nruns;
          r += (int64_t)gridDim.x * blockDim.x) {
         const int32_t j = run_start[r], je = run_start[r + 1];
         const u64 key = K2[j];
         const uint32_t meta = M2[j];
-        u64 s = mm_hash(key, meta) & mask;
+        const u64 h = mm_hash(key, meta);
+        atomicOr(bloom + ((h >> 32) & bmask), (1ULL << ((h >> 20) & 63)) | (1ULL << ((h >> 26) & 63)));
+        u64 s = h & mask;
         while (true) {
             uint32_t *w = reinterpret_cast<uint32_t *>(slots + 2 * s);
             if (atomicCAS(w + 2, MM_EMPTY, meta) == MM_EMPTY) {
@@ -1133,7 +1148,10 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
             t->mm = t->mm_buf;
             t->mm_mask = 0;
             t->mm_ent = (char *)t->mm_buf + 64;
+            t->mm_bloom = (u64 *)((char *)t->mm_buf + 96);
+            t->mm_bloom_mask = 0;
             cudaMemsetAsync(t->mm, 0xFF, 32, st);
+            cudaMemsetAsync(t->mm_bloom, 0, 8, st);
         }
         return rc;
     }
@@ -1177,17 +1195,23 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
     if (rc) { cudaFreeAsync(sc, st); cudaFreeAsync(eoff, st); return rc; }
     u64 slots = 2;
     while (slots < 2 * (u64)nruns) slots <<= 1;
-    const size_t pbytes = r16(32 * slots) + r16(16 * m);
+    u64 bwords = 1;
+    while (bwords * 64 < 8 * (u64)nruns) bwords <<= 1;
+    const size_t pbytes = r16(32 * slots) + r16(16 * m) + r16(8 * bwords);
     rc = cuda_check(cudaMallocAsync(&t->mm_buf, pbytes, st), "alloc multimap");
     if (rc) { cudaFreeAsync(sc, st); cudaFreeAsync(eoff, st); return rc; }
     t->mm = t->mm_buf;
     t->mm_mask = slots - 1;
     t->mm_ent = (char *)t->mm_buf + r16(32 * slots);
+    t->mm_bloom = (u64 *)((char *)t->mm_ent + r16(16 * m));
+    t->mm_bloom_mask = bwords - 1;
     t->bytes += (int64_t)pbytes;
     cudaMemsetAsync(t->mm, 0xFF, 32 * slots, st);
+    cudaMemsetAsync(t->mm_bloom, 0, 8 * bwords, st);
     int32_t *run_start = io;   // head flags are dead after the scan; io holds m + 1 ints >= nruns + 1
     k_mm_runs<<<gm, 256, 0, st>>>(K2, M2, P2, V, SV, P1, m, run_start, (ulonglong2 *)t->mm_ent);
-    k_mm_slots<<<grid_for(nruns, 256), 256, 0, st>>>(K2, M2, run_start, nruns, (ulonglong2 *)t->mm, t->mm_mask);
+    k_mm_slots<<<grid_for(nruns, 256), 256, 0, st>>>(K2, M2, run_start, nruns, (ulonglong2 *)t->mm, t->mm_mask,
+                                                         t->mm_bloom, t->mm_bloom_mask);
     cudaFreeAsync(sc, st);
     cudaFreeAsync(eoff, st);
     return cuda_check(cudaGetLastError(), "multimap kernels");
@@ -1322,7 +1346,8 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
     TabSpin tv{t->n, (const ulonglong2 *)t->keys, (const double2 *)t->logpsi, (const double2 *)t->psi_hat,
                t->slots, t->bucket_mask, t->shift_key, t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB,
                t->listA_b, t->listB_a, t->listA_idx, t->listB_idx, t->ah_keys, t->ah_vals, t->ah_mask,
-               (const ulonglong2 *)t->mm, t->mm_mask, (const ulonglong2 *)t->mm_ent, t->thr_single,
+               (const ulonglong2 *)t->mm, t->mm_mask, t->mm_bloom, t->mm_bloom_mask,
+               (const ulonglong2 *)t->mm_ent, t->thr_single,
                t->thr_double};
     const int64_t threads = n_rows * 32;
     int g = (int)std::min<int64_t>((threads + 255) / 256, 148 * 64);
@@ -1393,9 +1418,28 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
             const char *e = std::getenv("NNQS_MINB");
             minb = e ? std::atoi(e) : 44;
         }
+        static int dyn = -1;
+        if (dyn < 0) {
+            const char *e = std::getenv("NNQS_DYN");
+            dyn = e ? std::atoi(e) : 1;
+        }
+        unsigned long long *ctr = nullptr;
+        if (dyn) {
+            rc = cuda_check(cudaMallocAsync((void **)&ctr, 64, st), "alloc row counters");
+            if (rc) return rc;
+            cudaMemsetAsync(ctr, 0, 64, st);
+        }
+        int nl = 0;
         auto launch = [&](auto kern) {
-            kern<<<g, 256, 0, st>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc, (unsigned long long *)stats,
-                                    pairs, phase_mask, acc_heavy, t->thr_rowheavy, partial);
+            int gg = g;
+            if (dyn) {
+                int per_sm = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+                gg = std::max(1, per_sm) * 148;
+            }
+            kern<<<gg, 256, 0, st>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc, (unsigned long long *)stats,
+                                     pairs, phase_mask, acc_heavy, t->thr_rowheavy, partial, ctr ? ctr + nl : nullptr);
+            ++nl;
         };
         switch (minb / 10) {
             case 3: launch(k_eloc_spin<7, 3, false>); break;
@@ -1411,6 +1455,7 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
             default: launch(k_eloc_spin<8, 4, false>);
         }
         launch(k_eloc_spin<8, 4, true>);
+        if (ctr) cudaFreeAsync(ctr, st);
         cudaFreeAsync(partial, st);
     }
     if (acc_heavy) cudaFreeAsync(acc_heavy, st);
