@@ -57,6 +57,11 @@ struct SpinIndex {
     // x and x' in one (N_alpha, N_beta) sector, (-1)^{popc(x & F)} is a known
     // constant for F = the pair masks of X (-1 each) or a same-spin quad (+1),
     // so the strings Z and Z ^ F of a group merge into one.
+    // Diagonal group X = 0 in occupation form (all its strings have |Z| <= 2):
+    // sum_i d_i (-1)^{popc(x & Z_i)} = K + sum_{p occ} u_p + sum_{p<q occ} v_pq
+    bool diag_ok = false;
+    double diag_K = 0.0;
+    std::vector<double> diag_uv;      // [N + N*N]: u_p, then v (symmetric, zero diagonal)
     std::vector<uint32_t> foff;       // [K+1]
     std::vector<u64> fz;              // [M][2]
     std::vector<double> fd;           // [M]
@@ -79,6 +84,7 @@ struct DeviceHam {
     int32_t *pair_k[2] = {nullptr, nullptr};
     int32_t *quad_k[2] = {nullptr, nullptr};
     int32_t *ab_k = nullptr;
+    double *diag_uv = nullptr; // diagonal group in occupation form (structured path)
     uint32_t *foff = nullptr;  // folded table (structured path)
     void *fz = nullptr;
     double *fd = nullptr;

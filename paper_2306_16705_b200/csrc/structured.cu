@@ -78,6 +78,9 @@ struct SpinView {
     int64_t P;
     const int32_t *pair_k0, *pair_k1, *quad_k0, *quad_k1, *ab_k;
     int32_t diag_k;
+    int nq;                   // qubits
+    double diag_K;            // diagonal group in occupation form (SpinIndex), or
+    const double *diag_uv;    // nullptr: evaluate its Pauli strings
 };
 
 struct GroupView {
@@ -349,6 +352,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
     __shared__ uint8_t s_orb[WARPS_PER_BLOCK][4][64];   // occ(a), vir(a), occ(b), vir(b) of the row
     __shared__ int2 s_h[(PH & 8) ? WARPS_PER_BLOCK : 1][HCAP];   // heavy adjacent alpha groups (g, u rank)
     __shared__ RowState s_row[WARPS_PER_BLOCK];
+    __shared__ uint8_t s_oq[(PH & 1) ? WARPS_PER_BLOCK : 1][128];   // occupied qubits (diagonal)
     __shared__ double2 s_acc[WARPS_PER_BLOCK][32];
     if ((PH & 8) && !DIRECT && stats && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(stats, pairs);
     const int lane = threadIdx.x & 31;
@@ -442,8 +446,39 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
         };
         // ---- diagonal group: warp-cooperative Pauli sum, fixed reduction
         if ((PH & 1) && S.diag_k >= 0 && (phase_mask & 1)) {
-            const uint32_t gb = __ldg(G.goff + S.diag_k), ge = __ldg(G.goff + S.diag_k + 1);
-            const double hv = warp_strided_sum(G, gb, ge, rs->x0, rs->x1);
+            uint32_t gb = 0, ge = 0;
+            double hv;
+            if (S.diag_uv) {
+                // occupation form: K + sum_{p occ} u_p + sum_{p<q occ} v_pq over the
+                // row's occupied qubits (lane l: qubit l, l+32, .. and its partners above)
+                const int nocc = __popcll(rs->x0) + __popcll(rs->x1);
+                uint8_t *oq = s_oq[(PH & 1) ? (threadIdx.x >> 5) : 0];
+                __syncwarp();
+                for (int j = lane; j < S.nq; j += 32) {
+                    const u64 w = j < 64 ? rs->x0 : rs->x1;
+                    const int jb = j & 63;
+                    if ((w >> jb) & 1)
+                        oq[(j < 64 ? 0 : __popcll(rs->x0)) + __popcll(w & ((1ULL << jb) - 1))] = (uint8_t)j;
+                }
+                __syncwarp();
+                hv = 0.0;
+                for (int l = lane; l < nocc; l += 32) {
+                    const int p = oq[l];
+                    const double *vp = S.diag_uv + S.nq + (size_t)p * S.nq;
+                    double t = __ldg(S.diag_uv + p);
+                    for (int m = l + 1; m < nocc; ++m) t += __ldg(vp + oq[m]);
+                    hv += t;
+                }
+                for (int o = 16; o; o >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, o);
+                hv += S.diag_K;
+                gb = 0;
+                ge = (uint32_t)(nocc + nocc * (nocc - 1) / 2);
+                __syncwarp();
+            } else {
+                gb = __ldg(G.goff + S.diag_k);
+                ge = __ldg(G.goff + S.diag_k + 1);
+                hv = warp_strided_sum(G, gb, ge, rs->x0, rs->x1);
+            }
             if (lane == 0) {   // x' = x: psi_hat(x) (or 1 on the direct path)
                 double2 ps = make_double2(1.0, 0.0);
                 if (!DIRECT) ps = __ldg(T.psi_hat + i);
@@ -1064,6 +1099,44 @@ int nnqs_spin_index_build(const HostTable &H, SpinIndex &S) {
         }
         S.foff[k + 1] = (uint32_t)S.fd.size();
     }
+    // ---- diagonal group in occupation form (s_p = 1 - 2 n_p):
+    //   c0 + sum_p c_p s_p + sum_{p<q} c_pq s_p s_q
+    //   = K + sum_{p occ} u_p + sum_{p<q occ} v_pq,
+    //   K = c0 + sum c_p + sum c_pq,  u_p = -2 (c_p + sum_{q != p} c_pq),  v_pq = 4 c_pq
+    S.diag_ok = false;
+    if (S.diag_k >= 0 && N <= 128) {
+        std::vector<long double> c1(N, 0.0L), c2((size_t)N * N, 0.0L);
+        long double c0 = 0.0L;
+        bool ok = true;
+        for (int64_t t = H.off[S.diag_k]; t < H.off[S.diag_k + 1] && ok; ++t) {
+            int q[3], nb = 0;
+            for (int w = 0; w < 2; ++w)
+                for (u64 z = H.z[2 * t + w]; z; z &= z - 1) {
+                    if (nb == 2) { ok = false; break; }
+                    q[nb++] = 64 * w + __builtin_ctzll(z);
+                }
+            if (!ok) break;
+            if (nb == 0) c0 += H.d[t];
+            else if (nb == 1) c1[q[0]] += H.d[t];
+            else { c2[(size_t)q[0] * N + q[1]] += H.d[t]; c2[(size_t)q[1] * N + q[0]] += H.d[t]; }
+        }
+        if (ok) {
+            long double K = c0;
+            for (int p = 0; p < N; ++p) {
+                K += c1[p];
+                for (int q = p + 1; q < N; ++q) K += c2[(size_t)p * N + q];
+            }
+            S.diag_uv.assign((size_t)N + (size_t)N * N, 0.0);
+            for (int p = 0; p < N; ++p) {
+                long double R = 0.0L;
+                for (int q = 0; q < N; ++q) R += c2[(size_t)p * N + q];
+                S.diag_uv[p] = (double)(-2.0L * (c1[p] + R));
+                for (int q = 0; q < N; ++q) S.diag_uv[N + (size_t)p * N + q] = (double)(4.0L * c2[(size_t)p * N + q]);
+            }
+            S.diag_K = (double)K;
+            S.diag_ok = true;
+        }
+    }
     S.ok = true;
     return NNQS_OK;
 }
@@ -1085,6 +1158,12 @@ int nnqs_spin_index_upload(nnqs_ham h) {
     if ((rc = cuda_check(cudaMalloc((void **)&D.ab_k, bab), "alloc ab_k"))) return rc;
     if ((rc = cuda_check(cudaMemcpy(D.ab_k, S.ab_k.data(), bab, cudaMemcpyHostToDevice), "copy ab_k"))) return rc;
     D.bytes += (int64_t)bab;
+    if (S.diag_ok) {
+        const size_t bu = 8 * S.diag_uv.size();
+        if ((rc = cuda_check(cudaMalloc((void **)&D.diag_uv, bu), "alloc diag"))) return rc;
+        if ((rc = cuda_check(cudaMemcpy(D.diag_uv, S.diag_uv.data(), bu, cudaMemcpyHostToDevice), "copy diag"))) return rc;
+        D.bytes += (int64_t)bu;
+    }
     const size_t bo = 4 * S.foff.size(), bz = 8 * std::max<size_t>(S.fz.size(), 2), bd = 8 * std::max<size_t>(S.fd.size(), 1);
     if ((rc = cuda_check(cudaMalloc((void **)&D.foff, bo), "alloc foff"))) return rc;
     if ((rc = cuda_check(cudaMalloc((void **)&D.fz, bz), "alloc fz"))) return rc;
@@ -1107,6 +1186,8 @@ void nnqs_spin_index_release(nnqs_ham h) {
     }
     cudaFree(D.ab_k);
     D.ab_k = nullptr;
+    cudaFree(D.diag_uv);
+    D.diag_uv = nullptr;
     cudaFree(D.foff);
     cudaFree(D.fz);
     cudaFree(D.fd);
@@ -1341,7 +1422,8 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
                                   int64_t *stats, void *stream) {
     const SpinIndex &S = h->spin;
     const DeviceHam &D = h->dev;
-    SpinView sv{S.n, S.P, D.pair_k[0], D.pair_k[1], D.quad_k[0], D.quad_k[1], D.ab_k, S.diag_k};
+    SpinView sv{S.n, S.P, D.pair_k[0], D.pair_k[1], D.quad_k[0], D.quad_k[1], D.ab_k, S.diag_k,
+                h->host.n_qubits, S.diag_K, S.diag_ok ? D.diag_uv : nullptr};
     GroupView gv{D.foff, (const ulonglong2 *)D.fz, D.fd};   // in-sector folded strings
     TabSpin tv{t->n, (const ulonglong2 *)t->keys, (const double2 *)t->logpsi, (const double2 *)t->psi_hat,
                t->slots, t->bucket_mask, t->shift_key, t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB,
