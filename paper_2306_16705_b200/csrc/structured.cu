@@ -109,6 +109,8 @@ struct TabSpin {
     const u64 *mm_bloom;      // ~8 bits per run: most probes miss (C5: ~80%) and stop here, in L2
     u64 mm_bloom_mask;
     const ulonglong2 *mm_ent;  // {varying string, entry index} per multimap entry
+    const int32_t *nl_off;     // [alpha groups + 1] -> nl
+    const int4 *nl;            // {g', u rank, offA[g'], |list(g')|} of the present a' = a ^ u
     int32_t thr_single, thr_double;
 };
 
@@ -604,25 +606,23 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                 nheavy = 0;
                 __syncwarp();
             };
-            for (int c0 = 0; c0 < combos; c0 += 32) {
-                const int cidx = c0 + lane;
-                int p = 0, qo = 0;
-                int32_t g2 = -1;
-                if (cidx < combos) {
-                    p = occA[cidx / nva];
-                    qo = virA[cidx % nva];
-                    g2 = alpha_lookup(T, a ^ (1ULL << p) ^ (1ULL << qo));
+            (void)combos;
+            // the alpha strings a' = a ^ u present in the table, with their list ranges:
+            // precomputed once per alpha group by nnqs_table_prepare (k_nl_fill)
+            const int32_t nb0 = __ldg(T.nl_off + ga_row), nb1 = __ldg(T.nl_off + ga_row + 1);
+            for (int32_t c0 = nb0; c0 < nb1; c0 += 32) {
+                const int32_t cidx = c0 + lane;
+                int32_t g2 = -1, ljb = 0, llen = 0, urank = 0;
+                if (cidx < nb1) {
+                    const int4 nl = __ldg(T.nl + cidx);
+                    g2 = nl.x;
+                    urank = nl.y;
+                    ljb = nl.z;
+                    llen = nl.w;
                     ++c_cand;
-                }
-                // list ranges of the adjacent alpha strings, prefetched per lane
-                int32_t ljb = 0, llen = 0;
-                if (g2 >= 0) {
-                    ljb = __ldg(T.offA + g2);
-                    llen = __ldg(T.offA + g2 + 1) - ljb;
                 }
                 const bool heavy = g2 >= 0 && llen > T.thr_single;
                 const int32_t ll = (g2 >= 0 && !heavy) ? llen : 0;
-                const int32_t urank = g2 >= 0 ? (int32_t)pair_rank(min(p, qo), max(p, qo), S.n) : 0;
                 int32_t incl = ll;                       // warp prefix sum of the light list lengths
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -1000,6 +1000,43 @@ __global__ void k_hj_eval(SpinView S, GroupView G, TabSpin T, const int32_t *hea
     }
 }
 
+// Adjacent alpha strings of each alpha group g (a' = a ^ u, u = one occupied ->
+// one empty orbital, a' present in the table), warp per group, in (occupied,
+// empty) order.  FILL = false counts, FILL = true writes at nl_off[g].
+template <bool FILL>
+__global__ void k_nl(TabSpin T, int n_orb, int64_t n_groups, int32_t *count, const int32_t *nl_off, int4 *nl) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const u64 nmask = n_orb >= 64 ? ~0ULL : ((1ULL << n_orb) - 1);
+    for (int64_t g = warp; g < n_groups; g += nwarps) {
+        const u64 a = T.sa[T.listA_idx[T.offA[g]]];
+        const u64 va = ~a & nmask;
+        const int noa = __popcll(a), nva = __popcll(va);
+        const int combos = noa * nva;
+        int32_t pos = FILL ? nl_off[g] : 0;
+        for (int c0 = 0; c0 < combos; c0 += 32) {
+            const int c = c0 + lane;
+            int32_t g2 = -1;
+            int p = 0, q = 0;
+            if (c < combos) {
+                p = nth_set(a, c / nva);
+                q = nth_set(va, c % nva);
+                g2 = alpha_lookup(T, a ^ (1ULL << p) ^ (1ULL << q));
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, g2 >= 0);
+            if (FILL && g2 >= 0) {
+                const int32_t b0 = T.offA[g2];
+                nl[pos + __popc(m & lt_mask)] =
+                    make_int4(g2, pair_rank(min(p, q), max(p, q), n_orb), b0, T.offA[g2 + 1] - b0);
+            }
+            pos += __popc(m);
+        }
+        if (!FILL && lane == 0) count[g] = pos;
+    }
+}
+
 __global__ void k_find_heavy(const int32_t *listA_idx, const int32_t *ga_of, const int32_t *offA, int64_t n,
                              int32_t thr, int32_t *out, int *count) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
@@ -1361,12 +1398,50 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
         k_heads<<<g, 256, 0, st>>>(k1, n, flags);
         tb = tmp;
         cub::DeviceScan::InclusiveSum(ctmp, tb, flags, incl, (int)n, st);
-        if (pass == 0)
+        if (pass == 0) {
             k_csr<<<g, 256, 0, st>>>(k1, perm2, incl, n, t->sb, t->offA, t->ga_of, t->listA_b, t->listA_idx,
                                      t->ah_keys, t->ah_vals, t->ah_mask);
+            int32_t nga = 0;
+            rc = cuda_check(cudaMemcpyAsync(&nga, incl + n - 1, 4, cudaMemcpyDeviceToHost, st), "read alpha groups");
+            if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
+            if (rc) { cudaFreeAsync(scratch, st); return rc; }
+            t->n_alpha_groups = nga;
+        }
         else
             k_csr<<<g, 256, 0, st>>>(k1, perm2, incl, n, t->sa, t->offB, t->gb_of, t->listB_a, t->listB_idx,
                                      nullptr, nullptr, 0);
+    }
+    // adjacent-alpha lists per alpha group (phase (iii) streams them instead of
+    // repeating the 675 alpha-string lookups for every row of the group)
+    {
+        const int64_t ng = t->n_alpha_groups;
+        int32_t *cnt = nullptr;
+        rc = cuda_check(cudaMallocAsync((void **)&cnt, 4 * (ng + 1), st), "alloc nl counts");
+        if (rc) { cudaFreeAsync(scratch, st); return rc; }
+        TabSpin tv{};
+        tv.sa = t->sa; tv.listA_idx = t->listA_idx; tv.offA = t->offA;
+        tv.ah_keys = t->ah_keys; tv.ah_vals = t->ah_vals; tv.ah_mask = t->ah_mask;
+        const int n_orb = h->spin.n;
+        const int gw = (int)std::min<int64_t>((ng * 32 + 255) / 256, 148 * 32);
+        k_nl<false><<<std::max(gw, 1), 256, 0, st>>>(tv, n_orb, ng, cnt, nullptr, nullptr);
+        cudaMemsetAsync(cnt + ng, 0, 4, st);
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, cnt, (int)ng + 1, st);
+        void *stmp = nullptr;
+        rc = cuda_check(cudaMallocAsync(&stmp, tb, st), "alloc nl scan");
+        int32_t tot = 0;
+        if (!rc) {
+            cub::DeviceScan::ExclusiveSum(stmp, tb, cnt, cnt, (int)ng + 1, st);
+            rc = cuda_check(cudaMemcpyAsync(&tot, cnt + ng, 4, cudaMemcpyDeviceToHost, st), "read nl size");
+            if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
+            cudaFreeAsync(stmp, st);
+        }
+        if (!rc) rc = cuda_check(cudaMallocAsync(&t->nl_buf, 16 * ((size_t)tot + 1), st), "alloc nl");
+        if (rc) { cudaFreeAsync(cnt, st); cudaFreeAsync(scratch, st); return rc; }
+        t->nl_off = cnt;
+        t->nl = t->nl_buf;
+        t->bytes += 4 * (ng + 1) + 16 * ((int64_t)tot + 1);
+        k_nl<true><<<std::max(gw, 1), 256, 0, st>>>(tv, n_orb, ng, nullptr, t->nl_off, (int4 *)t->nl);
     }
     // deletion multimap for heavy groups (sorted CSR + unique-key hash)
     t->thr_single = 192;
@@ -1411,6 +1486,10 @@ void nnqs_table_release_spin(nnqs_table t) {
     if (t->spin_buf) cudaFreeAsync(t->spin_buf, (cudaStream_t)t->stream);
     if (t->mm_buf) cudaFreeAsync(t->mm_buf, (cudaStream_t)t->stream);
     if (t->heavy_groups) cudaFreeAsync(t->heavy_groups, (cudaStream_t)t->stream);
+    if (t->nl_off) cudaFreeAsync(t->nl_off, (cudaStream_t)t->stream);
+    if (t->nl_buf) cudaFreeAsync(t->nl_buf, (cudaStream_t)t->stream);
+    t->nl_off = nullptr;
+    t->nl = t->nl_buf = nullptr;
     t->heavy_groups = nullptr;
     t->n_heavy = 0;
     t->mm = t->mm_buf = nullptr;
@@ -1429,7 +1508,7 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
                t->slots, t->bucket_mask, t->shift_key, t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB,
                t->listA_b, t->listB_a, t->listA_idx, t->listB_idx, t->ah_keys, t->ah_vals, t->ah_mask,
                (const ulonglong2 *)t->mm, t->mm_mask, t->mm_bloom, t->mm_bloom_mask,
-               (const ulonglong2 *)t->mm_ent, t->thr_single,
+               (const ulonglong2 *)t->mm_ent, t->nl_off, (const int4 *)t->nl, t->thr_single,
                t->thr_double};
     const int64_t threads = n_rows * 32;
     int g = (int)std::min<int64_t>((threads + 255) / 256, 148 * 64);
