@@ -110,7 +110,8 @@ struct nnqs_table_s {
     u64 *slots = nullptr;     // hash slots [4 * n_buckets] (mode 0)
     u64 bucket_mask = 0;
     u64 *shift_key = nullptr; // device: order-preserving key of s = max Re logpsi
-    int *flag = nullptr;      // device: order violation flag
+    int *flag = nullptr;      // device: [0] order violation flag, [1] rows with psi_hat(x) < e^-600
+    int64_t n_direct = 0;     // host copy of flag[1]
     int64_t bytes = 0;
     // alpha/beta string index (structured path, mode 0)
     bool spin_ready = false;

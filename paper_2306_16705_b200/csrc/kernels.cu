@@ -154,11 +154,12 @@ __global__ void k_max_re(const double2 *lp, int64_t n, u64 *shift_key) {
     if ((threadIdx.x & 31) == 0 && m) atomicMax((unsigned long long *)shift_key, (unsigned long long)m);
 }
 
-__global__ void k_psi_hat(const double2 *lp, int64_t n, const u64 *shift_key, double2 *ph) {
+__global__ void k_psi_hat(const double2 *lp, int64_t n, const u64 *shift_key, double2 *ph, int *n_direct) {
     const double s = dkey_inv(*shift_key);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const double2 l = lp[i];
+        if (l.x > -INFINITY && l.x - s < -600.0) atomicAdd(n_direct, 1);   // rows on the exp-ratio path (R11)
         const double m = exp(l.x - s);
         double sn, cs;
         sincos(l.y, &sn, &cs);
@@ -471,14 +472,15 @@ int nnqs_table_build(nnqs_table t, const uint64_t *keys, const double *logpsi, v
     if (n) {
         k_max_re<<<grid_for(n, 256), 256, 0, st>>>((const double2 *)t->logpsi, n, t->shift_key);
         k_psi_hat<<<grid_for(n, 256), 256, 0, st>>>((const double2 *)t->logpsi, n, t->shift_key,
-                                                     (double2 *)t->psi_hat);
+                                                     (double2 *)t->psi_hat, t->flag + 1);
     }
     if ((rc = cuda_check(cudaGetLastError(), "table kernels"))) return rc;
-    if (t->mode == 0 && n > 1) {
-        int flag = 0;
-        if ((rc = cuda_check(cudaMemcpyAsync(&flag, t->flag, sizeof(int), cudaMemcpyDeviceToHost, st), "read flag"))) return rc;
+    if (n) {
+        int flag[2] = {0, 0};   // order violation, rows with psi_hat(x) < e^-600
+        if ((rc = cuda_check(cudaMemcpyAsync(flag, t->flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, st), "read flag"))) return rc;
         if ((rc = cuda_check(cudaStreamSynchronize(st), "sync"))) return rc;
-        if (flag) return nnqs_set_error(NNQS_E_TABLE, "keys are not strictly increasing as 128-bit integers");
+        t->n_direct = flag[1];
+        if (t->mode == 0 && flag[0]) return nnqs_set_error(NNQS_E_TABLE, "keys are not strictly increasing as 128-bit integers");
     }
     return NNQS_OK;
 }

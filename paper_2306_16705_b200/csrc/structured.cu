@@ -882,69 +882,90 @@ __global__ void k_mm_slots(const u64 *K2, const uint32_t *M2, const int32_t *run
 // the 1-deletions b'' - e_s in g's multimap (tag 0) and finds the rows (a, b)
 // with b - e_r = b'' - e_s.  Hits are emitted as (row, x' index) keys, sorted,
 // and summed per row in that order (k_hj_eval), so the result is deterministic.
+// Hit key of the join: (row - row_begin) << ibits | table index of x'; sorting
+// the keys on their used bits orders every row's hits by x' (deterministic sums).
 __global__ void __launch_bounds__(256) k_hj_emit(SpinView S, TabSpin T, const int32_t *heavy_groups, int n_heavy,
-                                                 int64_t row_begin, int64_t row_end, unsigned long long *counter,
-                                                 u64 *keys_out, int64_t cap, unsigned long long *stats) {
-    // block -> (heavy group, alpha single); threads -> entries of the neighbour's list
-    const int hg = blockIdx.x >> 10;
-    const int cidx = blockIdx.x & 1023;
+                                                 int64_t row_begin, int64_t row_end, int ibits, int kbits,
+                                                 unsigned long long *counter, u64 *keys_out, int64_t cap,
+                                                 unsigned long long *stats) {
+    // block -> (heavy group, one of its adjacent alpha strings a' (nl entry));
+    // threads -> (entry of list(a'), occupied beta orbital of the entry) pairs
+    const int hg = blockIdx.y;
     if (hg >= n_heavy) return;
-    const u64 nmask = S.n >= 64 ? ~0ULL : ((1ULL << S.n) - 1);
     const int32_t g = heavy_groups[hg];
-    const u64 a = T.sa[T.listA_idx[T.offA[g]]];
-    const u64 va = ~a & nmask;
-    const int nva = __popcll(va);
-    if (cidx >= __popcll(a) * nva) return;
-    const int p = nth_set(a, cidx / nva), q = nth_set(va, cidx % nva);
-    const int32_t g2 = alpha_lookup(T, a ^ (1ULL << p) ^ (1ULL << q));
-    if (g2 < 0) return;
-    const int32_t *abk = S.ab_k + pair_rank(min(p, q), max(p, q), S.n) * S.P;
-    const uint32_t meta = mm_meta(0, g);
-    const int32_t jb = T.offA[g2], je = T.offA[g2 + 1];
+    const int32_t nb0 = T.nl_off[g], nb1 = T.nl_off[g + 1];
+    const int lane = threadIdx.x & 31;
     unsigned long long probes = 0;
-    for (int32_t j = jb + threadIdx.x; j < je; j += blockDim.x) {
-        const u64 b2 = T.listA_b[j];
-        const int32_t idx2 = T.listA_idx[j];
-        for (u64 m1 = b2; m1; m1 &= m1 - 1) {
-            int32_t mb, me;
-            mm_find(T, b2 ^ (m1 & (~m1 + 1)), meta, mb, me);
-            ++probes;
+    for (int32_t c = nb0 + blockIdx.x; c < nb1; c += gridDim.x) {
+        const int4 nl = T.nl[c];
+        const int32_t *abk = S.ab_k + (int64_t)nl.y * S.P;
+        const uint32_t meta = mm_meta(0, g);
+        const int32_t jb = nl.z, len = nl.w;
+        const int nob = __popcll(T.listA_b[jb]);          // all entries of one table sector share it
+        const int64_t tasks = (int64_t)len * nob;
+        for (int64_t t0 = 0; t0 < tasks; t0 += blockDim.x) {
+            const int64_t t = t0 + threadIdx.x;
+            int32_t mb = 0, me = 0, idx2 = 0;
+            u64 b2 = 0;
+            if (t < tasks) {
+                const int32_t j = jb + (int32_t)(t / nob);
+                const int sb = (int)(t % nob);
+                b2 = T.listA_b[j];
+                idx2 = T.listA_idx[j];
+                mm_find(T, b2 ^ (1ULL << nth_set(b2, sb)), meta, mb, me);
+                ++probes;
+            }
             for (int32_t mj = mb; mj < me; ++mj) {
                 const ulonglong2 en = T.mm_ent[mj];
                 const int32_t e = (int32_t)en.y;
-                if (e < row_begin || e >= row_end) continue;
                 const u64 d = en.x ^ b2;
-                if (!d) continue;
-                const int r1 = __ffsll((long long)d) - 1, r2 = 63 - __clzll((long long)d);
-                if (abk[pair_rank(r1, r2, S.n)] < 0) continue;
-                const unsigned long long slot = atomicAdd(counter, 1ULL);
-                if ((int64_t)slot < cap) keys_out[slot] = ((u64)(e - row_begin) << 32) | (u64)(uint32_t)idx2;
+                bool ok = e >= row_begin && e < row_end && d != 0;
+                int32_t kk = -1;
+                if (ok) {
+                    const int r1 = __ffsll((long long)d) - 1, r2 = 63 - __clzll((long long)d);
+                    kk = abk[pair_rank(r1, r2, S.n)];
+                    ok = kk >= 0;
+                }
+                // warp-aggregated slot reservation among the lanes still in this loop
+                const unsigned act = __activemask();
+                const unsigned m = __ballot_sync(act, ok);
+                unsigned long long base = 0;
+                const int leader = __ffs(act) - 1;
+                if (lane == leader && m) base = atomicAdd(counter, (unsigned long long)__popc(m));
+                base = __shfl_sync(act, base, leader);
+                if (ok) {
+                    const unsigned long long slot = base + __popc(m & ((1u << lane) - 1u));
+                    if ((int64_t)slot < cap)
+                        keys_out[slot] = ((((u64)(e - row_begin) << ibits) | (u64)(uint32_t)idx2) << kbits) |
+                                         (kbits ? (u64)(uint32_t)kk : 0);
+                }
             }
         }
     }
     if (stats) {
         for (int o = 16; o; o >>= 1) probes += __shfl_xor_sync(0xffffffffu, probes, o);
-        if ((threadIdx.x & 31) == 0) atomicAdd(stats + 1, probes);
+        if (lane == 0) atomicAdd(stats + 1, probes);
     }
 }
 
-__device__ __forceinline__ int64_t lower_bound_u64(const u64 *a, int64_t n, u64 v) {
-    int64_t lo = 0, hi = n;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (a[mid] < v) lo = mid + 1; else hi = mid;
+// first / one-past-last position of every row's run in the sorted keys
+__global__ void k_hj_bounds(const u64 *keys, int64_t m, int shift, int32_t *kb, int32_t *ke) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+        const u64 r = keys[j] >> shift;
+        if (j == 0 || (keys[j - 1] >> shift) != r) kb[r] = (int32_t)j;
+        if (j == m - 1 || (keys[j + 1] >> shift) != r) ke[r] = (int32_t)(j + 1);
     }
-    return lo;
 }
 
 // one warp per row of the heavy groups: sum its sorted hits (fixed lane order)
 __global__ void k_hj_eval(SpinView S, GroupView G, TabSpin T, const int32_t *heavy_groups, int n_heavy,
-                          int64_t row_begin, int64_t row_end, const u64 *keys, int64_t m, double2 *acc,
-                          unsigned long long *stats) {
+                          int64_t row_begin, int64_t row_end, const u64 *keys, int ibits, int kbits, const int32_t *kb,
+                          const int32_t *ke, double2 *acc, unsigned long long *stats) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const double s = dkey_inv2(*T.shift_key);
+    const u64 imask = (1ULL << ibits) - 1, kmask = (1ULL << kbits) - 1;
     unsigned long long c_hit = 0, c_str = 0;
     for (int hg = 0; hg < n_heavy; ++hg) {
         const int32_t g = heavy_groups[hg];
@@ -953,19 +974,24 @@ __global__ void k_hj_eval(SpinView S, GroupView G, TabSpin T, const int32_t *hea
             const int32_t e = T.listA_idx[rb + t];
             if (e < row_begin || e >= row_end) continue;
             const u64 rloc = (u64)(e - row_begin);
-            const int64_t kb = lower_bound_u64(keys, m, rloc << 32);
-            const int64_t ke = lower_bound_u64(keys, m, (rloc + 1) << 32);
+            const int32_t hb = kb[rloc], he = ke[rloc];
             const ulonglong2 xk = T.keys[e];
             const u64 a = T.sa[e], b = T.sb[e];
             const double2 lx = T.logpsi[e];
             const bool direct = (lx.x - s) < -600.0;
             double ar = 0.0, ai = 0.0;
-            for (int64_t j = kb + lane; j < ke; j += 32) {
-                const int32_t idx = (int32_t)(uint32_t)keys[j];
-                const u64 du = a ^ T.sa[idx], dv = b ^ T.sb[idx];
-                const int p1 = __ffsll((long long)du) - 1, p2 = 63 - __clzll((long long)du);
-                const int r1 = __ffsll((long long)dv) - 1, r2 = 63 - __clzll((long long)dv);
-                const int32_t k = S.ab_k[pair_rank(p1, p2, S.n) * S.P + pair_rank(r1, r2, S.n)];
+            for (int32_t j = hb + lane; j < he; j += 32) {
+                const u64 key = keys[j];
+                const int32_t idx = (int32_t)((key >> kbits) & imask);
+                int32_t k;
+                if (kbits) {
+                    k = (int32_t)(key & kmask);       // group id carried in the key's low bits
+                } else {
+                    const u64 du = a ^ T.sa[idx], dv = b ^ T.sb[idx];
+                    const int p1 = __ffsll((long long)du) - 1, p2 = 63 - __clzll((long long)du);
+                    const int r1 = __ffsll((long long)dv) - 1, r2 = 63 - __clzll((long long)dv);
+                    k = S.ab_k[pair_rank(p1, p2, S.n) * S.P + pair_rank(r1, r2, S.n)];
+                }
                 const double hv = group_value1(G, k, xk.x, xk.y, c_str);
                 double2 ps;
                 if (!direct) {
@@ -1534,16 +1560,23 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
         if (rc) return rc;
         cudaMemsetAsync(acc_heavy, 0, 16 * n_rows, st);
         cudaMemsetAsync(hcnt, 0, 16, st);
-        const int hgrid = t->n_heavy * 1024;
+        int ibits = 1, rbits = 1;
+        while ((1LL << ibits) < t->n) ++ibits;
+        while ((1LL << rbits) < n_rows) ++rbits;
+        int kbits = 1;
+        while ((1LL << kbits) < h->n_groups) ++kbits;
+        if (rbits + ibits + kbits > 64) kbits = 0;   // no room: k is recomputed from the strings
+        const dim3 hgrid(512, t->n_heavy);
         int64_t cap = std::max<int64_t>(1 << 20, std::min<int64_t>((int64_t)1 << 26, 64 * n_rows));
         for (int attempt = 0; attempt < 2 && !rc; ++attempt) {
             size_t tb = 0;
-            cub::DeviceRadixSort::SortKeys(nullptr, tb, (const u64 *)nullptr, (u64 *)nullptr, (int)cap, 0, 64, st);
-            rc = cuda_check(cudaMallocAsync((void **)&hkeys, 16 * cap + tb + 64, st), "alloc hj keys");
+            cub::DeviceRadixSort::SortKeys(nullptr, tb, (const u64 *)nullptr, (u64 *)nullptr, (int)cap, kbits,
+                                           kbits + ibits + rbits, st);
+            rc = cuda_check(cudaMallocAsync((void **)&hkeys, 16 * cap + tb + 8 * n_rows + 1024, st), "alloc hj keys");
             if (rc) break;
             cudaMemsetAsync(hcnt, 0, 8, st);
-            k_hj_emit<<<hgrid, 256, 0, st>>>(sv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end, hcnt, hkeys,
-                                             cap, attempt == 0 ? (unsigned long long *)stats : nullptr);
+            k_hj_emit<<<hgrid, 256, 0, st>>>(sv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end, ibits, kbits, hcnt,
+                                             hkeys, cap, attempt == 0 ? (unsigned long long *)stats : nullptr);
             unsigned long long m = 0;
             rc = cuda_check(cudaMemcpyAsync(&m, hcnt, 8, cudaMemcpyDeviceToHost, st), "read hj count");
             if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
@@ -1556,12 +1589,17 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
             }
             if (m) {
                 u64 *k2 = hkeys + cap;
-                htmp = (void *)(hkeys + 2 * cap);
+                int32_t *kb = (int32_t *)(hkeys + 2 * cap), *ke = kb + n_rows;
+                htmp = (void *)(((uintptr_t)(ke + n_rows) + 511) & ~(uintptr_t)255);   // 256-B aligned
+                cudaMemsetAsync(kb, 0, 8 * n_rows, st);
                 tb = 0;
-                cub::DeviceRadixSort::SortKeys(nullptr, tb, (const u64 *)nullptr, (u64 *)nullptr, (int)m, 0, 64, st);
-                cub::DeviceRadixSort::SortKeys(htmp, tb, hkeys, k2, (int)m, 0, 64, st);
+                // order by (row, x' index) only: the group id rides along in the low bits
+                cub::DeviceRadixSort::SortKeys(nullptr, tb, (const u64 *)nullptr, (u64 *)nullptr, (int)m, kbits,
+                                               kbits + ibits + rbits, st);
+                cub::DeviceRadixSort::SortKeys(htmp, tb, hkeys, k2, (int)m, kbits, kbits + ibits + rbits, st);
+                k_hj_bounds<<<grid_for((int64_t)m, 256), 256, 0, st>>>(k2, (int64_t)m, ibits + kbits, kb, ke);
                 k_hj_eval<<<148 * 8, 256, 0, st>>>(sv, gv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end, k2,
-                                                   (int64_t)m, acc_heavy, (unsigned long long *)stats);
+                                                   ibits, kbits, kb, ke, acc_heavy, (unsigned long long *)stats);
             }
             break;
         }
@@ -1608,14 +1646,14 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
             case 6: launch(k_eloc_spin<7, 6, false>); break;
             default: launch(k_eloc_spin<7, 4, false>);
         }
-        launch(k_eloc_spin<7, 4, true>);
+        if (t->n_direct) launch(k_eloc_spin<7, 4, true>);
         switch (minb % 10) {
             case 3: launch(k_eloc_spin<8, 3, false>); break;
             case 5: launch(k_eloc_spin<8, 5, false>); break;
             case 6: launch(k_eloc_spin<8, 6, false>); break;
             default: launch(k_eloc_spin<8, 4, false>);
         }
-        launch(k_eloc_spin<8, 4, true>);
+        if (t->n_direct) launch(k_eloc_spin<8, 4, true>);
         if (ctr) cudaFreeAsync(ctr, st);
         cudaFreeAsync(partial, st);
     }
