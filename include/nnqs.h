@@ -158,6 +158,16 @@ int nnqs_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_
 int nnqs_set_algorithm(int algorithm);
 int nnqs_get_algorithm(void);
 
+/*
+ * Profiling aid (not part of the method): cycle counters of the structured
+ * kernel's sections, summed over warps, when libnnqs was compiled with
+ * -DNNQS_PROFILE (NNQS_NVCC_DEFINES); all zero otherwise.  out: host u64[16]
+ * = {diagonal, phase (i), phase (ii), (iii) list scans, (iii) heavy probes,
+ * hit flushes, row setup, total}; reset != 0 zeroes the device counters after
+ * reading.  Synchronises the device.  Returns NNQS_OK or NNQS_E_CUDA.
+ */
+int nnqs_debug_counters(uint64_t *out, int reset);
+
 /* Synchronises cuda_stream; NNQS_E_ZERO_PSI if any of eloc (device f64[n][2]) is NaN. */
 int nnqs_local_energy_check(const double *eloc, int64_t n, void *cuda_stream);
 

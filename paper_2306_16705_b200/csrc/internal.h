@@ -62,6 +62,12 @@ struct SpinIndex {
     bool diag_ok = false;
     double diag_K = 0.0;
     std::vector<double> diag_uv;      // [N + N*N]: u_p, then v (symmetric, zero diagonal)
+    // Single-excitation groups (alpha / beta pairs) in occupation form: their
+    // folded strings are B ^ {0 or one Z_R}, so the group value at an in-sector
+    // x is (-1)^{popc(x & B)} (T - 2 sum_{R occupied} c_R).  Record per pair
+    // slot (spin * P + pair rank): {B.lo, B.hi (as bits), T, 0, c_0 .. c_{N-1}}.
+    bool occ_ok = false;
+    std::vector<double> occ_rec;      // [2P][4 + N]
     std::vector<uint32_t> foff;       // [K+1]
     std::vector<u64> fz;              // [M][2]
     std::vector<double> fd;           // [M]
@@ -85,6 +91,7 @@ struct DeviceHam {
     int32_t *quad_k[2] = {nullptr, nullptr};
     int32_t *ab_k = nullptr;
     double *diag_uv = nullptr; // diagonal group in occupation form (structured path)
+    double *occ_rec = nullptr; // single-excitation groups in occupation form
     uint32_t *foff = nullptr;  // folded table (structured path)
     void *fz = nullptr;
     double *fd = nullptr;

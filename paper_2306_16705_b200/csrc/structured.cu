@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "internal.h"
 
@@ -79,6 +80,7 @@ struct SpinView {
     const int32_t *pair_k0, *pair_k1, *quad_k0, *quad_k1, *ab_k;
     int32_t diag_k;
     int nq;                   // qubits
+    const double *occ_rec;    // single-excitation records (SpinIndex::occ_rec) or nullptr
     double diag_K;            // diagonal group in occupation form (SpinIndex), or
     const double *diag_uv;    // nullptr: evaluate its Pauli strings
 };
@@ -206,6 +208,20 @@ __device__ __forceinline__ int32_t same_spin_group(const SpinView &S, int spin, 
     return __ldg((spin ? S.quad_k1 : S.quad_k0) + quad_rank(p1, p2, p3, p4));
 }
 
+// Queue tag of a same-spin excitation: singles with an occupation-form record
+// are queued as 0x80000000 | (spin * P + pair rank), everything else as k.
+#define OCC_TAG 0x80000000u
+__device__ __forceinline__ int32_t same_spin_tag(const SpinView &S, int spin, u64 d, int c) {
+    if (c == 2 && S.occ_rec) {
+        const int p1 = __ffsll((long long)d) - 1;
+        const int p2 = 63 - __clzll((long long)d);
+        const int32_t rk = pair_rank(p1, p2, S.n);
+        if (__ldg((spin ? S.pair_k1 : S.pair_k0) + rk) < 0) return -1;
+        return (int32_t)(OCC_TAG | (uint32_t)(spin * S.P + rk));
+    }
+    return same_spin_group(S, spin, d, c);
+}
+
 // multimap lookup: [beg, end) into mm_ent of the entries stored under (key, meta).
 // A slot is 32 B (one sector): {key, meta | beg << 32}, {end, -}.
 __device__ __forceinline__ void mm_find(const TabSpin &T, u64 key, uint32_t meta, int32_t &beg, int32_t &end) {
@@ -257,9 +273,10 @@ struct RowState {
 // psi_hat(x) < e^-600 (exp / sincos, large code) is a separate instantiation
 // (DIRECT), so this stays small and no ABI call forces the kernel's live
 // registers to local memory.
-template <bool DIRECT>
+template <bool DIRECT, bool OCC>
 __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *psi_hat, const double2 *logpsi,
-                                             int2 *q, int qn, int cnt, const RowState *rs, double2 *acc) {
+                                             int2 *q, int qn, int cnt, const RowState *rs, double2 *acc,
+                                             const double *occ_rec, int nq) {
     const int lane = threadIdx.x & 31;
     uint32_t c_hit = 0, c_str = 0;
     __syncwarp();
@@ -268,10 +285,14 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
     int2 e = make_int2(-1, 0);
     uint32_t gb0 = 0, ge0 = 0;
     double2 ps0 = make_double2(0.0, 0.0);
+    bool occ = false;
     if (lane < cnt) {
         e = q[lane];
-        gb0 = __ldg(G.goff + e.x);
-        ge0 = __ldg(G.goff + e.x + 1);
+        occ = OCC && e.x < 0;                      // single excitation, occupation-form record
+        if (!occ) {
+            gb0 = __ldg(G.goff + e.x);
+            ge0 = __ldg(G.goff + e.x + 1);
+        }
         if (!direct) ps0 = __ldg(psi_hat + e.y);   // issued with the offsets, used after the sum
         ++c_hit;
     }
@@ -290,8 +311,21 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
         a.y = fma(hv, ps.y, a.y);
         acc[lane] = a;
     };
-    const bool big = lane < cnt && ge0 - gb0 > 32;
-    if (lane < cnt && !big) {
+    if (OCC && occ) {
+        // (-1)^{popc(x & B)} (T - 2 sum_{R occupied} c_R): the folded strings B ^ Z_R summed
+        // in occupation form (SpinIndex::occ_rec)
+        const double *rr = occ_rec + (size_t)(e.x & 0x7FFFFFFF) * (4 + nq);
+        const u64 B0 = (u64)__double_as_longlong(__ldg(rr)), B1 = (u64)__double_as_longlong(__ldg(rr + 1));
+        const double Tg = __ldg(rr + 2);
+        double sum = 0.0;
+        for (u64 w = x0; w; w &= w - 1) sum += __ldg(rr + 4 + (__ffsll((long long)w) - 1));
+        for (u64 w = x1; w; w &= w - 1) sum += __ldg(rr + 68 + (__ffsll((long long)w) - 1));
+        const double hv = flip_sign2(fma(-2.0, sum, Tg), (__popcll(x0 & B0) + __popcll(x1 & B1)) & 1);
+        c_str += __popcll(x0) + __popcll(x1) + 1;
+        add(hv, e.y);
+    }
+    const bool big = lane < cnt && !occ && ge0 - gb0 > 32;
+    if (lane < cnt && !occ && !big) {
         // 4 strings in flight per lane (loads issued before the sums; same order)
         double hv = 0.0;
         for (uint32_t i0 = gb0; i0 < ge0; i0 += 4) {
@@ -326,6 +360,22 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
     __syncwarp();
     return make_uint2(c_hit, c_str);
 }
+
+// section cycle counters (build with -DNNQS_PROFILE; nnqs_debug_counters)
+#ifdef NNQS_PROFILE
+__device__ unsigned long long g_prof[16];
+#define PROF_DECL unsigned long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#define PROF_T(v) const long long v = clock64();
+#define PROF_ADD(slot, v) prof[slot] += (unsigned long long)(clock64() - (v));
+#define PROF_FLUSH                                                            \
+    if ((threadIdx.x & 31) == 0)                                              \
+        for (int ps_ = 0; ps_ < 12; ++ps_) atomicAdd(g_prof + ps_, prof[ps_]);
+#else
+#define PROF_DECL
+#define PROF_T(v)
+#define PROF_ADD(slot, v)
+#define PROF_FLUSH
+#endif
 
 #define SCAN_LIMIT 8192
 #define WARPS_PER_BLOCK 8
@@ -377,7 +427,12 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
         if (lane == 0) v = atomicAdd(row_ctr, 1ULL);
         return (int64_t)__shfl_sync(0xffffffffu, v, 0);
     };
+    PROF_DECL
     for (int64_t r = row_ctr ? next_row(0) : warp; r < n_rows; r = next_row(r)) {
+        PROF_T(t_row)
+#ifdef NNQS_PROFILE
+        bool prof_in_ss = false;
+#endif
         const int64_t i = row_begin + r;
         const double2 lx0 = T.logpsi[i];
         if (!(lx0.x > -INFINITY)) {
@@ -405,14 +460,19 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
         __syncwarp();
         int qn = 0;                                  // warp-uniform queue length
         auto flush = [&](int cnt) {                  // lanes < cnt evaluate q[lane]
-            const uint2 fo = flush_queue<DIRECT>(G, T.psi_hat, T.logpsi, q, qn, cnt, rs, acc);
+            PROF_T(t_fl)
+            const uint2 fo = flush_queue<DIRECT, (PH & 6) != 0>(G, T.psi_hat, T.logpsi, q, qn, cnt, rs, acc, S.occ_rec, S.nq);
             c_hit += fo.x;
             c_str += fo.y;
             qn -= cnt;
+            PROF_ADD(5, t_fl)
+#ifdef NNQS_PROFILE
+            if (prof_in_ss) prof[9] += (unsigned long long)(clock64() - t_fl);
+#endif
         };
-        auto push = [&](int32_t k, int32_t idx) {    // all lanes; k < 0 = no hit
-            const unsigned m = __ballot_sync(0xffffffffu, k >= 0);
-            if (k >= 0) q[qn + __popc(m & lt_mask)] = make_int2(k, idx);
+        auto push = [&](int32_t k, int32_t idx) {    // all lanes; k == -1 = no hit (OCC_TAG keys are negative)
+            const unsigned m = __ballot_sync(0xffffffffu, k != -1);
+            if (k != -1) q[qn + __popc(m & lt_mask)] = make_int2(k, idx);
             qn += __popc(m);
             if (qn >= 32) flush(32);
         };
@@ -446,6 +506,8 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                 push(k, idx);
             }
         };
+        PROF_ADD(6, t_row)
+        PROF_T(t_diag)
         // ---- diagonal group: warp-cooperative Pauli sum, fixed reduction
         if ((PH & 1) && S.diag_k >= 0 && (phase_mask & 1)) {
             uint32_t gb = 0, ge = 0;
@@ -492,9 +554,14 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                 ++c_hit;
             }
         }
+        PROF_ADD(0, t_diag)
         // ---- (i) same beta string: x' = (a'', b), a'' in A(b);  (ii) same alpha string
         for (int ph = 0; ph < 2; ++ph) {
             if (!(PH & (2 << ph)) || !(phase_mask & (2 << ph))) continue;
+            PROF_T(t_ph)
+#ifdef NNQS_PROFILE
+            prof_in_ss = true;
+#endif
             const int32_t g = ph == 0 ? T.gb_of[i] : T.ga_of[i];
             const int32_t *off = ph == 0 ? T.offB : T.offA;
             const u64 *lst = ph == 0 ? T.listB_a : T.listA_b;
@@ -517,12 +584,13 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         const u64 d = mine ^ v[u];
                         const int c = __popcll(d);
                         int32_t k = -1;
-                        if ((c == 2 || c == 4) && 2 * __popcll(mine & d) == c) k = same_spin_group(S, ph, d, c);
+                        if ((c == 2 || c == 4) && 2 * __popcll(mine & d) == c) k = same_spin_tag(S, ph, d, c);
                         c_cand += j < je;
                         push(k, ix[u]);
                     }
                 }
             } else {
+                PROF_T(t_ssh)
                 // heavy group: 1-deletion (singles) and 2-deletion (doubles) probes
                 const int no = __popcll(mine);
                 const int ntask = no + no * (no - 1) / 2;
@@ -554,11 +622,17 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         const ulonglong2 en = __ldg(T.mm_ent + mj);
                         idx = (int32_t)en.y;
                         const u64 d = mine ^ en.x;
-                        if (__popcll(d) == swant) k = same_spin_group(S, ph, d, swant);
+                        if (__popcll(d) == swant) k = same_spin_tag(S, ph, d, swant);
                     });
                 }
+                PROF_ADD(8, t_ssh)
             }
+            PROF_ADD(1 + ph, t_ph)
         }
+        PROF_T(t_iii)
+#ifdef NNQS_PROFILE
+        prof_in_ss = false;
+#endif
         // ---- (iii) alpha single u x beta single v
         const int32_t ga_row = T.ga_of[i];
         const bool row_heavy = (PH & 8) && acc_heavy && (T.offA[ga_row + 1] - T.offA[ga_row] > thr_rowheavy);
@@ -580,6 +654,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             // heavy alpha groups a' = a ^ u: probe (a', b - e_r) for every occupied beta r,
             // nheavy x nob probes spread over the lanes, matches drained warp-wide
             auto probe_heavy = [&]() {
+                PROF_T(t_hv)
                 __syncwarp();
                 const int ntask = nheavy * nob;
                 for (int t0 = 0; t0 < ntask; t0 += 32) {
@@ -605,6 +680,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                 }
                 nheavy = 0;
                 __syncwarp();
+                PROF_ADD(4, t_hv)
             };
             (void)combos;
             // the alpha strings a' = a ^ u present in the table, with their list ranges:
@@ -674,6 +750,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             probe_heavy();
         }
         if (qn > 0) flush(qn);
+        PROF_ADD(3, t_iii)
         __syncwarp();
         double ar = acc[lane].x, ai = acc[lane].y;
         const double2 lx = rs->lx;
@@ -697,7 +774,9 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             }
             out[r] = e;
         }
+        PROF_ADD(7, t_row)
     }
+    PROF_FLUSH
     if (stats) {
         for (int o = 16; o; o >>= 1) {
             c_cand += __shfl_xor_sync(0xffffffffu, c_cand, o);
@@ -1162,6 +1241,40 @@ int nnqs_spin_index_build(const HostTable &H, SpinIndex &S) {
         }
         S.foff[k + 1] = (uint32_t)S.fd.size();
     }
+    // ---- single-excitation groups in occupation form (see SpinIndex::occ_rec)
+    S.occ_ok = N <= 128;
+    if (S.occ_ok) {
+        const int stride = 4 + N;
+        S.occ_rec.assign((size_t)2 * S.P * stride, 0.0);
+        for (int sp = 0; sp < 2 && S.occ_ok; ++sp)
+            for (int64_t rk = 0; rk < S.P && S.occ_ok; ++rk) {
+                const int32_t k = S.pair_k[sp][rk];
+                if (k < 0) continue;
+                // base B = bitwise majority of the group's strings (the JW string J of
+                // the pair; every other string is J ^ Z_R)
+                int cnt[128] = {0};
+                const uint32_t ns = S.foff[k + 1] - S.foff[k];
+                for (uint32_t t = S.foff[k]; t < S.foff[k + 1]; ++t)
+                    for (int w = 0; w < 2; ++w)
+                        for (u64 z = S.fz[2 * t + w]; z; z &= z - 1) ++cnt[64 * w + __builtin_ctzll(z)];
+                u64 B0 = 0, B1 = 0;
+                for (int j = 0; j < 128; ++j)
+                    if (2 * (uint32_t)cnt[j] > ns) (j < 64 ? B0 : B1) |= 1ULL << (j & 63);
+                double *rec = &S.occ_rec[((size_t)sp * S.P + rk) * stride];
+                long double Tg = 0.0L;
+                for (uint32_t t = S.foff[k]; t < S.foff[k + 1]; ++t) {
+                    const u64 w0 = S.fz[2 * t] ^ B0, w1 = S.fz[2 * t + 1] ^ B1;
+                    const int pc = __builtin_popcountll(w0) + __builtin_popcountll(w1);
+                    if (pc > 1) { S.occ_ok = false; break; }
+                    Tg += S.fd[t];
+                    if (pc == 1) rec[4 + (w0 ? __builtin_ctzll(w0) : 64 + __builtin_ctzll(w1))] += S.fd[t];
+                }
+                std::memcpy(&rec[0], &B0, 8);
+                std::memcpy(&rec[1], &B1, 8);
+                rec[2] = (double)Tg;
+            }
+        if (!S.occ_ok) S.occ_rec.clear();
+    }
     // ---- diagonal group in occupation form (s_p = 1 - 2 n_p):
     //   c0 + sum_p c_p s_p + sum_{p<q} c_pq s_p s_q
     //   = K + sum_{p occ} u_p + sum_{p<q occ} v_pq,
@@ -1221,6 +1334,12 @@ int nnqs_spin_index_upload(nnqs_ham h) {
     if ((rc = cuda_check(cudaMalloc((void **)&D.ab_k, bab), "alloc ab_k"))) return rc;
     if ((rc = cuda_check(cudaMemcpy(D.ab_k, S.ab_k.data(), bab, cudaMemcpyHostToDevice), "copy ab_k"))) return rc;
     D.bytes += (int64_t)bab;
+    if (S.occ_ok) {
+        const size_t bo2 = 8 * S.occ_rec.size();
+        if ((rc = cuda_check(cudaMalloc((void **)&D.occ_rec, bo2), "alloc occ"))) return rc;
+        if ((rc = cuda_check(cudaMemcpy(D.occ_rec, S.occ_rec.data(), bo2, cudaMemcpyHostToDevice), "copy occ"))) return rc;
+        D.bytes += (int64_t)bo2;
+    }
     if (S.diag_ok) {
         const size_t bu = 8 * S.diag_uv.size();
         if ((rc = cuda_check(cudaMalloc((void **)&D.diag_uv, bu), "alloc diag"))) return rc;
@@ -1251,6 +1370,8 @@ void nnqs_spin_index_release(nnqs_ham h) {
     D.ab_k = nullptr;
     cudaFree(D.diag_uv);
     D.diag_uv = nullptr;
+    cudaFree(D.occ_rec);
+    D.occ_rec = nullptr;
     cudaFree(D.foff);
     cudaFree(D.fz);
     cudaFree(D.fd);
@@ -1528,7 +1649,7 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
     const SpinIndex &S = h->spin;
     const DeviceHam &D = h->dev;
     SpinView sv{S.n, S.P, D.pair_k[0], D.pair_k[1], D.quad_k[0], D.quad_k[1], D.ab_k, S.diag_k,
-                h->host.n_qubits, S.diag_K, S.diag_ok ? D.diag_uv : nullptr};
+                h->host.n_qubits, S.occ_ok ? D.occ_rec : nullptr, S.diag_K, S.diag_ok ? D.diag_uv : nullptr};
     GroupView gv{D.foff, (const ulonglong2 *)D.fz, D.fd};   // in-sector folded strings
     TabSpin tv{t->n, (const ulonglong2 *)t->keys, (const double2 *)t->logpsi, (const double2 *)t->psi_hat,
                t->slots, t->bucket_mask, t->shift_key, t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB,
@@ -1661,4 +1782,21 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
     if (hcnt) cudaFreeAsync(hcnt, st);
     if (hkeys) cudaFreeAsync(hkeys, st);
     return cuda_check(cudaGetLastError(), "structured local energy launch");
+}
+
+int nnqs_debug_counters(uint64_t *out, int reset) {
+    if (!out) return nnqs_set_error(NNQS_E_ARG, "nnqs_debug_counters: null out");
+    for (int i = 0; i < 16; ++i) out[i] = 0;
+#ifdef NNQS_PROFILE
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 16);
+    if (e == cudaSuccess && reset) {
+        unsigned long long z[16] = {0};
+        e = cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+    }
+    if (e != cudaSuccess) return nnqs_set_error(NNQS_E_CUDA, cudaGetErrorString(e));
+#else
+    (void)reset;
+#endif
+    return NNQS_OK;
 }

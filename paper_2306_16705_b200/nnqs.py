@@ -37,6 +37,7 @@ _sig = {
     "nnqs_local_energy_check": ([P, I64, P], ctypes.c_int),
     "nnqs_set_algorithm": ([ctypes.c_int], ctypes.c_int),
     "nnqs_get_algorithm": ([], ctypes.c_int),
+    "nnqs_debug_counters": ([P, ctypes.c_int], ctypes.c_int),
     "nnqs_energy_chunk_partials": ([P, P, I64, P, P, P], ctypes.c_int),
     "nnqs_energy_combine": ([P, I64, ctypes.c_int, P, P], ctypes.c_int),
     "nnqs_energy_reduce": ([P, P, I64, P, P], ctypes.c_int),
@@ -217,6 +218,13 @@ def nnqs_set_algorithm(algorithm: int):
 
 def nnqs_get_algorithm() -> int:
     return int(_lib.nnqs_get_algorithm())
+
+
+def nnqs_debug_counters(reset: bool = True):
+    """Section cycle counters of the structured kernel (libnnqs built with -DNNQS_PROFILE)."""
+    out = np.zeros(16, dtype=np.uint64)
+    _check(_lib.nnqs_debug_counters(out.ctypes.data, int(bool(reset))))
+    return out
 
 
 def nnqs_local_energy_check(eloc, stream=None):

@@ -27,3 +27,10 @@ for it in range(3):
     s = stats.cpu().numpy()
     print(f"algo={algo} C{c} rows={n} K={ham.info()['n_groups']} {ms:.3f} ms  rows/s={n/ms*1e3:.3e} pairs/s={n*ham.info()['n_groups']/ms*1e3:.3e} stats={s} hits/row={s[2]/n:.1f}")
 e0.record(); tab2 = nnqs.nnqs_table_prepare(ham, 0, keys, lp); e1.record(); e1.synchronize(); print("table_prepare ms", e0.elapsed_time(e1))
+if os.environ.get("NNQS_PRINT_PROF"):
+    nnqs.nnqs_debug_counters(True)
+    nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, eloc_out=out)
+    pc = nnqs.nnqs_debug_counters(True).astype(float)
+    names = ["diag", "phase_i", "phase_ii", "iii_total", "iii_heavy", "flush", "setup", "row_total", "ss_heavy", "ss_flush"]
+    tot = pc[7] or 1.0
+    print("section cycles (share of row total):", {k: round(v / tot, 3) for k, v in zip(names, pc[:10])})
