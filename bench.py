@@ -138,15 +138,24 @@ def profile_traffic():
     if not os.path.exists(TRAFFIC_FILE):
         return None
     tot, kernels = 0.0, []
+    alu_w, t_w = 0.0, 0.0
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     for block in open(TRAFFIC_FILE).read().split("## ")[1:]:
         name = block.splitlines()[0].strip()
+        if name in kernels:            # the capture may run into the next call: first launch of each
+            continue
         for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             m = re.search(re.escape(key) + r" = ([0-9.]+) (\w+)", block)
             if m:
                 tot += float(m.group(1)) * scale.get(m.group(2), 1)
+        mt = re.search(r"gpu__time_duration.sum = ([0-9.]+) ms", block)
+        ma = re.search(r"sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active = ([0-9.]+) %", block)
+        if mt and ma:
+            alu_w += float(mt.group(1)) * float(ma.group(1))
+            t_w += float(mt.group(1))
         kernels.append(name)
-    return {"bytes_per_launch": tot, "kernels": kernels, "source": os.path.relpath(TRAFFIC_FILE, ROOT)}
+    return {"bytes_per_launch": tot, "kernels": kernels, "source": os.path.relpath(TRAFFIC_FILE, ROOT),
+            "ncu_alu_pipe_pct_time_weighted": (alu_w / t_w) if t_w else None}
 
 
 def cpu_baseline(mol, st, n_rows_req, seconds_target=15.0):
