@@ -1687,7 +1687,13 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
         int kbits = 1;
         while ((1LL << kbits) < h->n_groups) ++kbits;
         if (rbits + ibits + kbits > 64) kbits = 0;   // no room: k is recomputed from the strings
-        const dim3 hgrid(512, t->n_heavy);
+        static int hj_gx = -1, hj_ev = -1;   // grid shapes (tuning: NNQS_HJ_GX, NNQS_HJ_EV)
+        if (hj_gx < 0) {
+            const char *e1 = std::getenv("NNQS_HJ_GX"), *e2 = std::getenv("NNQS_HJ_EV");
+            hj_gx = e1 ? std::atoi(e1) : 512;
+            hj_ev = e2 ? std::atoi(e2) : 8;
+        }
+        const dim3 hgrid(hj_gx, t->n_heavy);
         int64_t cap = std::max<int64_t>(1 << 20, std::min<int64_t>((int64_t)1 << 26, 64 * n_rows));
         for (int attempt = 0; attempt < 2 && !rc; ++attempt) {
             size_t tb = 0;
@@ -1719,7 +1725,7 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
                                                kbits + ibits + rbits, st);
                 cub::DeviceRadixSort::SortKeys(htmp, tb, hkeys, k2, (int)m, kbits, kbits + ibits + rbits, st);
                 k_hj_bounds<<<grid_for((int64_t)m, 256), 256, 0, st>>>(k2, (int64_t)m, ibits + kbits, kb, ke);
-                k_hj_eval<<<148 * 8, 256, 0, st>>>(sv, gv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end, k2,
+                k_hj_eval<<<148 * hj_ev, 256, 0, st>>>(sv, gv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end, k2,
                                                    ibits, kbits, kb, ke, acc_heavy, (unsigned long long *)stats);
             }
             break;
