@@ -259,6 +259,8 @@ __device__ __forceinline__ void nth_pair(int c, int &i, int &j) {
 // (views by value, accumulators in/out): a reference argument of a call that
 // is not inlined forces the referenced object -- e.g. a kernel-parameter
 // struct -- into local memory.
+#define QCAP 256   // per-warp hit ring (power of two >= 32 + 4 * 32)
+
 // The row being evaluated by a warp, and its per-lane accumulators, live in
 // shared memory: they are touched only here and at the row's start and end,
 // which keeps the scanning loops' register footprint (and spills) down.
@@ -275,7 +277,7 @@ struct RowState {
 // registers to local memory.
 template <bool DIRECT, bool OCC>
 __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *psi_hat, const double2 *logpsi,
-                                             int2 *q, int qn, int cnt, const RowState *rs, double2 *acc,
+                                             const int2 *q, int qh, int cnt, const RowState *rs, double2 *acc,
                                              const double *occ_rec, int nq) {
     const int lane = threadIdx.x & 31;
     uint32_t c_hit = 0, c_str = 0;
@@ -287,7 +289,7 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
     double2 ps0 = make_double2(0.0, 0.0);
     bool occ = false;
     if (lane < cnt) {
-        e = q[lane];
+        e = q[(qh + lane) & (QCAP - 1)];          // ring buffer: no shifting after a flush
         occ = OCC && e.x < 0;                      // single excitation, occupation-form record
         if (!occ) {
             gb0 = __ldg(G.goff + e.x);
@@ -356,8 +358,6 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
         }
     }
     __syncwarp();
-    if (lane < qn - cnt) q[lane] = q[lane + cnt];
-    __syncwarp();
     return make_uint2(c_hit, c_str);
 }
 
@@ -382,7 +382,6 @@ __device__ unsigned long long g_prof[16];
 #ifndef NNQS_SPIN_MINB
 #define NNQS_SPIN_MINB 4
 #endif
-#define QCAP 64
 #define HCAP 96
 
 // one warp per row; rows are table entries [row_begin, row_begin + n_rows).
@@ -458,12 +457,13 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             else virB[j - __popcll(b & below)] = (uint8_t)j;
         }
         __syncwarp();
-        int qn = 0;                                  // warp-uniform queue length
-        auto flush = [&](int cnt) {                  // lanes < cnt evaluate q[lane]
+        int qn = 0, qh = 0;                          // warp-uniform ring length and head
+        auto flush = [&](int cnt) {                  // lanes < cnt evaluate q[qh + lane]
             PROF_T(t_fl)
-            const uint2 fo = flush_queue<DIRECT, (PH & 6) != 0>(G, T.psi_hat, T.logpsi, q, qn, cnt, rs, acc, S.occ_rec, S.nq);
+            const uint2 fo = flush_queue<DIRECT, (PH & 6) != 0>(G, T.psi_hat, T.logpsi, q, qh, cnt, rs, acc, S.occ_rec, S.nq);
             c_hit += fo.x;
             c_str += fo.y;
+            qh = (qh + cnt) & (QCAP - 1);
             qn -= cnt;
             PROF_ADD(5, t_fl)
 #ifdef NNQS_PROFILE
@@ -472,9 +472,20 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
         };
         auto push = [&](int32_t k, int32_t idx) {    // all lanes; k == -1 = no hit (OCC_TAG keys are negative)
             const unsigned m = __ballot_sync(0xffffffffu, k != -1);
-            if (k != -1) q[qn + __popc(m & lt_mask)] = make_int2(k, idx);
+            if (k != -1) q[(qh + qn + __popc(m & lt_mask)) & (QCAP - 1)] = make_int2(k, idx);
             qn += __popc(m);
             if (qn >= 32) flush(32);
+        };
+        // four candidates per lane at once (same queue order as four push calls:
+        // u-major, then lane), one flush check
+        auto push4 = [&](const int32_t *kk, const int32_t *ix) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const unsigned m = __ballot_sync(0xffffffffu, kk[u] != -1);
+                if (kk[u] != -1) q[(qh + qn + __popc(m & lt_mask)) & (QCAP - 1)] = make_int2(kk[u], ix[u]);
+                qn += __popc(m);
+            }
+            while (qn >= 32) flush(32);
         };
         // Every lane holds a multimap match range [mb, me) and a tag; all matches of
         // the warp are evaluated 32 at a time in (lane, position) order -- parallel
@@ -578,16 +589,17 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         v[u] = j < je ? __ldg(lst + j) : mine;
                         ix[u] = j < je ? __ldg(lidx + j) : 0;
                     }
+                    int32_t kk[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < 4; ++u) {           // group-id loads of all four issued before any push
                         const int32_t j = j0 + 32 * u + lane;
                         const u64 d = mine ^ v[u];
                         const int c = __popcll(d);
-                        int32_t k = -1;
-                        if ((c == 2 || c == 4) && 2 * __popcll(mine & d) == c) k = same_spin_tag(S, ph, d, c);
+                        kk[u] = -1;
+                        if ((c == 2 || c == 4) && 2 * __popcll(mine & d) == c) kk[u] = same_spin_tag(S, ph, d, c);
                         c_cand += j < je;
-                        push(k, ix[u]);
                     }
+                    push4(kk, ix);
                 }
             } else {
                 PROF_T(t_ssh)
@@ -728,18 +740,19 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         v[u] = f < total ? __ldg(T.listA_b + jj[u]) : b;
                         ix[u] = f < total ? __ldg(T.listA_idx + jj[u]) : 0;   // issued with v: no dependent load on a hit
                     }
+                    int32_t kk[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < 4; ++u) {           // group-id loads of all four issued before any push
                         const u64 d = b ^ v[u];
-                        int32_t k = -1;
+                        kk[u] = -1;
                         if (__popcll(d) == 2 && __popcll(b & d) == 1) {
                             const int r1 = __ffsll((long long)d) - 1;
                             const int r2 = 63 - __clzll((long long)d);
-                            k = __ldg(S.ab_k + (int64_t)ur[u] * S.P + pair_rank(r1, r2, S.n));
+                            kk[u] = __ldg(S.ab_k + (int64_t)ur[u] * S.P + pair_rank(r1, r2, S.n));
                         }
                         c_cand += (f0 + 32 * u + lane) < total;
-                        push(k, ix[u]);
                     }
+                    push4(kk, ix);
                 }
                 // heavy adjacent alpha strings: deferred to the warp's heavy list
                 const unsigned hb = __ballot_sync(0xffffffffu, heavy && !(phase_mask & 32));
