@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             rs->lx = lx0;
             rs->direct = DIRECT;
         }
-        acc[lane] = (PH == 8 && lane == 0) ? partial[r] : make_double2(0.0, 0.0);
+        acc[lane] = ((PH & 16) && lane == 0) ? partial[r] : make_double2(0.0, 0.0);   // 16: continue a row
         for (int j = lane; j < S.n; j += 32) {       // orbital lists (replace nth-set-bit searches)
             const u64 below = (1ULL << j) - 1;
             if ((a >> j) & 1) occA[__popcll(a & below)] = (uint8_t)j;
@@ -1780,20 +1780,21 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
                                      pairs, phase_mask, acc_heavy, t->thr_rowheavy, partial, ctr ? ctr + nl : nullptr);
             ++nl;
         };
+        // three launches, each a smaller kernel (instruction cache): diagonal + phase (i)
+        // -> partial; phase (ii) adds; phase (iii) adds and finalises
         switch (minb / 10) {
-            case 3: launch(k_eloc_spin<7, 3, false>); break;
-            case 5: launch(k_eloc_spin<7, 5, false>); break;
-            case 6: launch(k_eloc_spin<7, 6, false>); break;
-            default: launch(k_eloc_spin<7, 4, false>);
+            case 3: launch(k_eloc_spin<3, 3, false>); launch(k_eloc_spin<20, 3, false>); break;
+            default: launch(k_eloc_spin<3, 4, false>); launch(k_eloc_spin<20, 4, false>);
         }
-        if (t->n_direct) launch(k_eloc_spin<7, 4, true>);
+        if (t->n_direct) {
+            launch(k_eloc_spin<3, 4, true>);
+            launch(k_eloc_spin<20, 4, true>);
+        }
         switch (minb % 10) {
-            case 3: launch(k_eloc_spin<8, 3, false>); break;
-            case 5: launch(k_eloc_spin<8, 5, false>); break;
-            case 6: launch(k_eloc_spin<8, 6, false>); break;
-            default: launch(k_eloc_spin<8, 4, false>);
+            case 3: launch(k_eloc_spin<24, 3, false>); break;
+            default: launch(k_eloc_spin<24, 4, false>);
         }
-        if (t->n_direct) launch(k_eloc_spin<8, 4, true>);
+        if (t->n_direct) launch(k_eloc_spin<24, 4, true>);
         if (ctr) cudaFreeAsync(ctr, st);
         cudaFreeAsync(partial, st);
     }
