@@ -195,6 +195,22 @@ def test_c5_full_launch_sampled(nnqs, dev, c5):
     assert s[0] == n * ham.info()["n_groups"] and s[2] > n
 
 
+def test_c5_bitwise_determinism_and_slices(nnqs, dev, c5):
+    """C5 at full size: the same bits on a re-run and when the rows are split
+    into uneven slices (the rank slices of a multi-GPU run) -- covers the
+    entry-driven join of the heavy alpha group, the multimap probes and the
+    dynamic row schedule (a row's summation order depends on the row alone)."""
+    m, st, ham, tab = c5
+    n = len(st.keys)
+    a = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n).cpu().numpy()
+    b = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n).cpu().numpy()
+    cuts = [0, 123457, 500001, 777777, n]
+    d = np.concatenate([nnqs.nnqs_local_energy(ham, tab, s0, n_rows=s1 - s0).cpu().numpy()
+                        for s0, s1 in zip(cuts[:-1], cuts[1:])])
+    assert a.tobytes() == b.tobytes()
+    assert a.tobytes() == d.tobytes()
+
+
 def test_c5_structured_equals_literal_hits(nnqs, dev, c5):
     """On a 4096-row slice of C5: identical hit counts for the two enumerations
     (the same (row, group) pairs are found), E_loc within tolerance of each
