@@ -36,7 +36,7 @@ UNIT = "local energies/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5", choices=["C4", "C5"])
@@ -403,6 +403,8 @@ def run_ours(args):
             "compress_s": round(compress_s, 3)}),
         "coupled_terms_per_s": n * K * args.steps / t_total,
         "local_energy_kernel_ms": kern_avg_ms,
+        "step_ms": [round(v, 3) for v in step_ms],
+        "local_energy_ms": [round(v, 3) for v in kern_ms],
         "kernel_share_of_step": kern_avg_ms / (1e3 * t_total / args.steps),
         "energy": {"mean_re": float(energy[0]), "mean_im": float(energy[1]), "var": float(energy[2]),
                    "W": float(energy[3])},

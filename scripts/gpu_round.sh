@@ -9,5 +9,5 @@ timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?" >> gpurun_out/rc.txt
 if [ "${NCU:-1}" = "1" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/b_ncu.log 2>&1; echo "ncu-list rc=$?" >> gpurun_out/rc.txt
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_eloc_spin|k_hj" -c 6 -f -o gpurun_out/le_full python scripts/time_kernel.py 5 > gpurun_out/ncu_full.log 2>&1; echo "ncu-full rc=$?" >> gpurun_out/rc.txt
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_eloc_spin|k_hj" -c 7 -f -o gpurun_out/le_full python scripts/time_kernel.py 5 > gpurun_out/ncu_full.log 2>&1; echo "ncu-full rc=$?" >> gpurun_out/rc.txt
 fi
