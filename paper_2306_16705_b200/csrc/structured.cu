@@ -980,57 +980,88 @@ __global__ void __launch_bounds__(256) k_hj_emit(SpinView S, TabSpin T, const in
                                                  int64_t row_begin, int64_t row_end, int ibits, int kbits,
                                                  unsigned long long *counter, u64 *keys_out, int64_t cap,
                                                  unsigned long long *stats) {
-    // block -> (heavy group, one of its adjacent alpha strings a' (nl entry));
-    // threads -> (entry of list(a'), occupied beta orbital of the entry) pairs
+    // (heavy group g = blockIdx.y): the tasks (adjacent alpha string a', entry of
+    // list(a'), occupied beta orbital of the entry) of all of g's adjacent strings
+    // are flattened through a block-local prefix sum and spread over the whole grid
+    // (list lengths differ by 100x: one block per a' left most SMs idle)
     const int hg = blockIdx.y;
     if (hg >= n_heavy) return;
     const int32_t g = heavy_groups[hg];
     const int32_t nb0 = T.nl_off[g], nb1 = T.nl_off[g + 1];
+    const int nc = nb1 - nb0;                        // <= n_alpha * n_empty <= 1024 (n <= 64)
+    __shared__ long long s_pre[1025];
+    __shared__ int4 s_nl[1024];
+    __shared__ int s_nob[1024];
+    typedef cub::BlockScan<long long, 256> Scan;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    long long cnt4[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int c = 4 * threadIdx.x + u;
+        cnt4[u] = 0;
+        if (c < nc) {
+            const int4 nl = T.nl[nb0 + c];
+            const int nob = __popcll(T.listA_b[nl.z]);     // all entries of one table sector share it
+            s_nl[c] = nl;
+            s_nob[c] = nob;
+            cnt4[u] = (long long)nl.w * nob;
+        }
+    }
+    long long tot = 0;
+    Scan(scan_tmp).ExclusiveSum(cnt4, cnt4, tot);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        if (4 * threadIdx.x + u < nc) s_pre[4 * threadIdx.x + u] = cnt4[u];
+    if (threadIdx.x == 0) s_pre[nc] = tot;
+    __syncthreads();
     const int lane = threadIdx.x & 31;
+    const uint32_t meta = mm_meta(0, g);
     unsigned long long probes = 0;
-    for (int32_t c = nb0 + blockIdx.x; c < nb1; c += gridDim.x) {
-        const int4 nl = T.nl[c];
-        const int32_t *abk = S.ab_k + (int64_t)nl.y * S.P;
-        const uint32_t meta = mm_meta(0, g);
-        const int32_t jb = nl.z, len = nl.w;
-        const int nob = __popcll(T.listA_b[jb]);          // all entries of one table sector share it
-        const int64_t tasks = (int64_t)len * nob;
-        for (int64_t t0 = 0; t0 < tasks; t0 += blockDim.x) {
-            const int64_t t = t0 + threadIdx.x;
-            int32_t mb = 0, me = 0, idx2 = 0;
-            u64 b2 = 0;
-            if (t < tasks) {
-                const int32_t j = jb + (int32_t)(t / nob);
-                const int sb = (int)(t % nob);
-                b2 = T.listA_b[j];
-                idx2 = T.listA_idx[j];
-                mm_find(T, b2 ^ (1ULL << nth_set(b2, sb)), meta, mb, me);
-                ++probes;
+    for (long long t0 = (long long)blockIdx.x * blockDim.x; t0 < tot; t0 += (long long)gridDim.x * blockDim.x) {
+        const long long t = t0 + threadIdx.x;
+        int32_t mb = 0, me = 0, idx2 = 0;
+        u64 b2 = 0;
+        const int32_t *abk = S.ab_k;
+        if (t < tot) {
+            int lo = 0, hi = nc;                         // last c with s_pre[c] <= t
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_pre[mid] <= t) lo = mid; else hi = mid;
             }
-            for (int32_t mj = mb; mj < me; ++mj) {
-                const ulonglong2 en = T.mm_ent[mj];
-                const int32_t e = (int32_t)en.y;
-                const u64 d = en.x ^ b2;
-                bool ok = e >= row_begin && e < row_end && d != 0;
-                int32_t kk = -1;
-                if (ok) {
-                    const int r1 = __ffsll((long long)d) - 1, r2 = 63 - __clzll((long long)d);
-                    kk = abk[pair_rank(r1, r2, S.n)];
-                    ok = kk >= 0;
-                }
-                // warp-aggregated slot reservation among the lanes still in this loop
-                const unsigned act = __activemask();
-                const unsigned m = __ballot_sync(act, ok);
-                unsigned long long base = 0;
-                const int leader = __ffs(act) - 1;
-                if (lane == leader && m) base = atomicAdd(counter, (unsigned long long)__popc(m));
-                base = __shfl_sync(act, base, leader);
-                if (ok) {
-                    const unsigned long long slot = base + __popc(m & ((1u << lane) - 1u));
-                    if ((int64_t)slot < cap)
-                        keys_out[slot] = ((((u64)(e - row_begin) << ibits) | (u64)(uint32_t)idx2) << kbits) |
-                                         (kbits ? (u64)(uint32_t)kk : 0);
-                }
+            const int4 nl = s_nl[lo];
+            const int nob = s_nob[lo];
+            const long long loc = t - s_pre[lo];
+            const int32_t j = nl.z + (int32_t)(loc / nob);
+            const int sb = (int)(loc % nob);
+            abk = S.ab_k + (int64_t)nl.y * S.P;
+            b2 = T.listA_b[j];
+            idx2 = T.listA_idx[j];
+            mm_find(T, b2 ^ (1ULL << nth_set(b2, sb)), meta, mb, me);
+            ++probes;
+        }
+        for (int32_t mj = mb; mj < me; ++mj) {
+            const ulonglong2 en = T.mm_ent[mj];
+            const int32_t e = (int32_t)en.y;
+            const u64 d = en.x ^ b2;
+            bool ok = e >= row_begin && e < row_end && d != 0;
+            int32_t kk = -1;
+            if (ok) {
+                const int r1 = __ffsll((long long)d) - 1, r2 = 63 - __clzll((long long)d);
+                kk = abk[pair_rank(r1, r2, S.n)];
+                ok = kk >= 0;
+            }
+            // warp-aggregated slot reservation among the lanes still in this loop
+            const unsigned act = __activemask();
+            const unsigned m = __ballot_sync(act, ok);
+            unsigned long long base = 0;
+            const int leader = __ffs(act) - 1;
+            if (lane == leader && m) base = atomicAdd(counter, (unsigned long long)__popc(m));
+            base = __shfl_sync(act, base, leader);
+            if (ok) {
+                const unsigned long long slot = base + __popc(m & ((1u << lane) - 1u));
+                if ((int64_t)slot < cap)
+                    keys_out[slot] = ((((u64)(e - row_begin) << ibits) | (u64)(uint32_t)idx2) << kbits) |
+                                     (kbits ? (u64)(uint32_t)kk : 0);
             }
         }
     }
@@ -1703,7 +1734,7 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
         static int hj_gx = -1, hj_ev = -1;   // grid shapes (tuning: NNQS_HJ_GX, NNQS_HJ_EV)
         if (hj_gx < 0) {
             const char *e1 = std::getenv("NNQS_HJ_GX"), *e2 = std::getenv("NNQS_HJ_EV");
-            hj_gx = e1 ? std::atoi(e1) : 512;
+            hj_gx = e1 ? std::atoi(e1) : 1184;
             hj_ev = e2 ? std::atoi(e2) : 8;
         }
         const dim3 hgrid(hj_gx, t->n_heavy);
