@@ -111,7 +111,7 @@ struct TabSpin {
     const u64 *mm_bloom;      // ~8 bits per run: most probes miss (C5: ~80%) and stop here, in L2
     u64 mm_bloom_mask;
     const ulonglong2 *mm_ent;  // {varying string, entry index} per multimap entry
-    const int32_t *nl_off;     // [alpha groups + 1] -> nl
+    const int2 *nl_rng;        // [alpha groups] -> [begin, end) in nl
     const int4 *nl;            // {g', u rank, offA[g'], |list(g')|} of the present a' = a ^ u
     int32_t thr_single, thr_double;
 };
@@ -697,7 +697,8 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             (void)combos;
             // the alpha strings a' = a ^ u present in the table, with their list ranges:
             // precomputed once per alpha group by nnqs_table_prepare (k_nl_fill)
-            const int32_t nb0 = __ldg(T.nl_off + ga_row), nb1 = __ldg(T.nl_off + ga_row + 1);
+            const int2 nbr = __ldg(T.nl_rng + ga_row);
+            const int32_t nb0 = nbr.x, nb1 = nbr.y;
             for (int32_t c0 = nb0; c0 < nb1; c0 += 32) {
                 const int32_t cidx = c0 + lane;
                 int32_t g2 = -1, ljb = 0, llen = 0, urank = 0;
@@ -987,7 +988,7 @@ __global__ void __launch_bounds__(256) k_hj_emit(SpinView S, TabSpin T, const in
     const int hg = blockIdx.y;
     if (hg >= n_heavy) return;
     const int32_t g = heavy_groups[hg];
-    const int32_t nb0 = T.nl_off[g], nb1 = T.nl_off[g + 1];
+    const int32_t nb0 = T.nl_rng[g].x, nb1 = T.nl_rng[g].y;
     const int nc = nb1 - nb0;                        // <= n_alpha * n_empty <= 1024 (n <= 64)
     __shared__ long long s_pre[1025];
     __shared__ int4 s_nl[1024];
@@ -1151,9 +1152,11 @@ __global__ void k_hj_eval(SpinView S, GroupView G, TabSpin T, const int32_t *hea
 
 // Adjacent alpha strings of each alpha group g (a' = a ^ u, u = one occupied ->
 // one empty orbital, a' present in the table), warp per group, in (occupied,
-// empty) order.  FILL = false counts, FILL = true writes at nl_off[g].
-template <bool FILL>
-__global__ void k_nl(TabSpin T, int n_orb, int64_t n_groups, int32_t *count, const int32_t *nl_off, int4 *nl) {
+// empty) order.
+__global__ void k_nl(TabSpin T, int n_orb, int64_t n_groups, int2 *rng, int4 *nl, unsigned long long *cursor) {
+    // pass 1 counts the present a', one atomic reserves the group's block, pass 2
+    // (the same probes, now cache-hot) writes it: one launch, no host round trip.
+    // Block positions depend on scheduling; each group's list (and its order) does not.
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -1164,7 +1167,17 @@ __global__ void k_nl(TabSpin T, int n_orb, int64_t n_groups, int32_t *count, con
         const u64 va = ~a & nmask;
         const int noa = __popcll(a), nva = __popcll(va);
         const int combos = noa * nva;
-        int32_t pos = FILL ? nl_off[g] : 0;
+        int32_t cnt = 0;
+        for (int c0 = 0; c0 < combos; c0 += 32) {
+            const int c = c0 + lane;
+            int32_t g2 = -1;
+            if (c < combos) g2 = alpha_lookup(T, a ^ (1ULL << nth_set(a, c / nva)) ^ (1ULL << nth_set(va, c % nva)));
+            cnt += __popc(__ballot_sync(0xffffffffu, g2 >= 0));
+        }
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(cursor, (unsigned long long)cnt);
+        int32_t pos = (int32_t)__shfl_sync(0xffffffffu, base, 0);
+        if (lane == 0) rng[g] = make_int2(pos, pos + cnt);
         for (int c0 = 0; c0 < combos; c0 += 32) {
             const int c = c0 + lane;
             int32_t g2 = -1;
@@ -1175,14 +1188,13 @@ __global__ void k_nl(TabSpin T, int n_orb, int64_t n_groups, int32_t *count, con
                 g2 = alpha_lookup(T, a ^ (1ULL << p) ^ (1ULL << q));
             }
             const unsigned m = __ballot_sync(0xffffffffu, g2 >= 0);
-            if (FILL && g2 >= 0) {
+            if (g2 >= 0) {
                 const int32_t b0 = T.offA[g2];
                 nl[pos + __popc(m & lt_mask)] =
                     make_int4(g2, pair_rank(min(p, q), max(p, q), n_orb), b0, T.offA[g2 + 1] - b0);
             }
             pos += __popc(m);
         }
-        if (!FILL && lane == 0) count[g] = pos;
     }
 }
 
@@ -1606,33 +1618,22 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
     // repeating the 675 alpha-string lookups for every row of the group)
     {
         const int64_t ng = t->n_alpha_groups;
-        int32_t *cnt = nullptr;
-        rc = cuda_check(cudaMallocAsync((void **)&cnt, 4 * (ng + 1), st), "alloc nl counts");
+        const int n_orb = h->spin.n;
+        const int64_t maxc = (int64_t)(n_orb / 2) * (n_orb - n_orb / 2);   // max occupied x empty
+        const size_t rb = (8 * (size_t)ng + 15) & ~size_t(15);            // 16-B aligned regions
+        const size_t bytes = rb + 64 + 16 * (size_t)(ng * maxc + 1);
+        rc = cuda_check(cudaMallocAsync(&t->nl_buf, bytes, st), "alloc nl");
         if (rc) { cudaFreeAsync(scratch, st); return rc; }
+        t->nl_rng = t->nl_buf;
+        unsigned long long *cursor = (unsigned long long *)((char *)t->nl_buf + rb);
+        t->nl = (char *)t->nl_buf + rb + 64;
+        t->bytes += (int64_t)bytes;
+        cudaMemsetAsync(cursor, 0, 8, st);
         TabSpin tv{};
         tv.sa = t->sa; tv.listA_idx = t->listA_idx; tv.offA = t->offA;
         tv.ah_keys = t->ah_keys; tv.ah_vals = t->ah_vals; tv.ah_mask = t->ah_mask;
-        const int n_orb = h->spin.n;
         const int gw = (int)std::min<int64_t>((ng * 32 + 255) / 256, 148 * 32);
-        k_nl<false><<<std::max(gw, 1), 256, 0, st>>>(tv, n_orb, ng, cnt, nullptr, nullptr);
-        cudaMemsetAsync(cnt + ng, 0, 4, st);
-        size_t tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, cnt, (int)ng + 1, st);
-        void *stmp = nullptr;
-        rc = cuda_check(cudaMallocAsync(&stmp, tb, st), "alloc nl scan");
-        int32_t tot = 0;
-        if (!rc) {
-            cub::DeviceScan::ExclusiveSum(stmp, tb, cnt, cnt, (int)ng + 1, st);
-            rc = cuda_check(cudaMemcpyAsync(&tot, cnt + ng, 4, cudaMemcpyDeviceToHost, st), "read nl size");
-            if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
-            cudaFreeAsync(stmp, st);
-        }
-        if (!rc) rc = cuda_check(cudaMallocAsync(&t->nl_buf, 16 * ((size_t)tot + 1), st), "alloc nl");
-        if (rc) { cudaFreeAsync(cnt, st); cudaFreeAsync(scratch, st); return rc; }
-        t->nl_off = cnt;
-        t->nl = t->nl_buf;
-        t->bytes += 4 * (ng + 1) + 16 * ((int64_t)tot + 1);
-        k_nl<true><<<std::max(gw, 1), 256, 0, st>>>(tv, n_orb, ng, nullptr, t->nl_off, (int4 *)t->nl);
+        k_nl<<<std::max(gw, 1), 256, 0, st>>>(tv, n_orb, ng, (int2 *)t->nl_rng, (int4 *)t->nl, cursor);
     }
     // deletion multimap for heavy groups (sorted CSR + unique-key hash)
     t->thr_single = 192;
@@ -1677,9 +1678,8 @@ void nnqs_table_release_spin(nnqs_table t) {
     if (t->spin_buf) cudaFreeAsync(t->spin_buf, (cudaStream_t)t->stream);
     if (t->mm_buf) cudaFreeAsync(t->mm_buf, (cudaStream_t)t->stream);
     if (t->heavy_groups) cudaFreeAsync(t->heavy_groups, (cudaStream_t)t->stream);
-    if (t->nl_off) cudaFreeAsync(t->nl_off, (cudaStream_t)t->stream);
     if (t->nl_buf) cudaFreeAsync(t->nl_buf, (cudaStream_t)t->stream);
-    t->nl_off = nullptr;
+    t->nl_rng = nullptr;
     t->nl = t->nl_buf = nullptr;
     t->heavy_groups = nullptr;
     t->n_heavy = 0;
@@ -1699,7 +1699,7 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
                t->slots, t->bucket_mask, t->shift_key, t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB,
                t->listA_b, t->listB_a, t->listA_idx, t->listB_idx, t->ah_keys, t->ah_vals, t->ah_mask,
                (const ulonglong2 *)t->mm, t->mm_mask, t->mm_bloom, t->mm_bloom_mask,
-               (const ulonglong2 *)t->mm_ent, t->nl_off, (const int4 *)t->nl, t->thr_single,
+               (const ulonglong2 *)t->mm_ent, (const int2 *)t->nl_rng, (const int4 *)t->nl, t->thr_single,
                t->thr_double};
     const int64_t threads = n_rows * 32;
     int g = (int)std::min<int64_t>((threads + 255) / 256, 148 * 64);
