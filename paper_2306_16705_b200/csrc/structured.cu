@@ -874,7 +874,7 @@ __device__ __forceinline__ int mm_keys_of(int32_t la, int32_t lb, int na, int nb
     int c = 0;
     if (la > thr_s) c += nb;
     if (la > thr_d) c += nb * (nb - 1) / 2;
-    if (lb > thr_s) c += na;
+    if (lb > thr_d) c += na;                 // beta groups are probed (phase (i)) only above thr_d
     if (lb > thr_d) c += na * (na - 1) / 2;
     return c;
 }
@@ -904,7 +904,7 @@ __global__ void k_mm_emit(const u64 *sa, const u64 *sb, const int32_t *ga_of, co
             const u64 w = side == 0 ? sb[e] : sa[e];
             const int32_t g = side == 0 ? ga : gb;
             const int tag = side == 0 ? 0 : 2;
-            if (len <= thr_s) continue;
+            if (len <= (side == 0 ? thr_s : thr_d)) continue;   // alpha groups: also phase (iii) neighbours
             for (u64 m1 = w; m1; m1 &= m1 - 1) {
                 const u64 b1 = m1 & (~m1 + 1);
                 K[o] = w ^ b1; M[o] = mm_meta(tag, g); V[o] = (int32_t)e; SV[o] = w; ++o;
