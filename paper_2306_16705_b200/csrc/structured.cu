@@ -1514,8 +1514,13 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
     rc = cuda_check(cudaMemcpyAsync(&nruns, P1 + m - 1, 4, cudaMemcpyDeviceToHost, st), "read runs");
     if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
     if (rc) { cudaFreeAsync(sc, st); cudaFreeAsync(eoff, st); return rc; }
+    static double mm_load = -1.0;   // slots >= mm_load * runs (power of two); tuning: NNQS_MM_LOAD
+    if (mm_load < 0) {
+        const char *e = std::getenv("NNQS_MM_LOAD");
+        mm_load = e ? std::atof(e) : 4.0;   // measured: 2 -> 69.6, 3 -> 68.6, 5 -> 68.4, 9 -> 68.8 ms/step
+    }
     u64 slots = 2;
-    while (slots < 2 * (u64)nruns) slots <<= 1;
+    while ((double)slots < mm_load * (double)nruns) slots <<= 1;
     u64 bwords = 1;
     while (bwords * 64 < 8 * (u64)nruns) bwords <<= 1;
     const size_t pbytes = r16(32 * slots) + r16(16 * m) + r16(8 * bwords);
