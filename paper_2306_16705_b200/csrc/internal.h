@@ -146,6 +146,7 @@ struct nnqs_table_s {
     int64_t n_alpha_groups = 0;
     void *nl_rng = nullptr;                    // int2 [n_alpha_groups]: adjacent-alpha list range (structured.cu k_nl)
     void *nl = nullptr;                        // int4 {g', u rank, offA[g'], len}
+    int32_t *nl_cost = nullptr;                // [n_alpha_groups] phase (iii) work estimate of a row
     void *nl_buf = nullptr;
     int n_heavy = 0;
 };

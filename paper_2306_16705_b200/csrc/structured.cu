@@ -398,7 +398,8 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                                                    int64_t n_rows, double2 *out,
                                                    unsigned long long *stats, unsigned long long pairs,
                                                    int phase_mask, const double2 *acc_heavy, int32_t thr_rowheavy,
-                                                   double2 *partial, unsigned long long *row_ctr) {
+                                                   double2 *partial, unsigned long long *row_ctr,
+                                                   const int32_t *perm) {
     __shared__ int2 s_q[WARPS_PER_BLOCK][QCAP];
     __shared__ uint8_t s_orb[WARPS_PER_BLOCK][4][64];   // occ(a), vir(a), occ(b), vir(b) of the row
     __shared__ int2 s_h[(PH & 8) ? WARPS_PER_BLOCK : 1][HCAP];   // heavy adjacent alpha groups (g, u rank)
@@ -424,7 +425,8 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
         if (!row_ctr) return cur + nwarps;
         unsigned long long v = 0;
         if (lane == 0) v = atomicAdd(row_ctr, 1ULL);
-        return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+        const int64_t w = (int64_t)__shfl_sync(0xffffffffu, v, 0);
+        return (perm && w < n_rows) ? (int64_t)__ldg(perm + w) : w;   // costliest rows first
     };
     PROF_DECL
     for (int64_t r = row_ctr ? next_row(0) : warp; r < n_rows; r = next_row(r)) {
@@ -1153,7 +1155,8 @@ __global__ void k_hj_eval(SpinView S, GroupView G, TabSpin T, const int32_t *hea
 // Adjacent alpha strings of each alpha group g (a' = a ^ u, u = one occupied ->
 // one empty orbital, a' present in the table), warp per group, in (occupied,
 // empty) order.
-__global__ void k_nl(TabSpin T, int n_orb, int64_t n_groups, int2 *rng, int4 *nl, unsigned long long *cursor) {
+__global__ void k_nl(TabSpin T, int n_orb, int64_t n_groups, int2 *rng, int4 *nl, unsigned long long *cursor,
+                     int32_t thr_single, int32_t *cost) {
     // pass 1 counts the present a', one atomic reserves the group's block, pass 2
     // (the same probes, now cache-hot) writes it: one launch, no host round trip.
     // Block positions depend on scheduling; each group's list (and its order) does not.
@@ -1178,6 +1181,7 @@ __global__ void k_nl(TabSpin T, int n_orb, int64_t n_groups, int2 *rng, int4 *nl
         if (lane == 0) base = atomicAdd(cursor, (unsigned long long)cnt);
         int32_t pos = (int32_t)__shfl_sync(0xffffffffu, base, 0);
         if (lane == 0) rng[g] = make_int2(pos, pos + cnt);
+        int32_t work = 0;                            // phase (iii) work estimate of a row of g
         for (int c0 = 0; c0 < combos; c0 += 32) {
             const int c = c0 + lane;
             int32_t g2 = -1;
@@ -1189,12 +1193,30 @@ __global__ void k_nl(TabSpin T, int n_orb, int64_t n_groups, int2 *rng, int4 *nl
             }
             const unsigned m = __ballot_sync(0xffffffffu, g2 >= 0);
             if (g2 >= 0) {
-                const int32_t b0 = T.offA[g2];
-                nl[pos + __popc(m & lt_mask)] =
-                    make_int4(g2, pair_rank(min(p, q), max(p, q), n_orb), b0, T.offA[g2 + 1] - b0);
+                const int32_t b0 = T.offA[g2], len = T.offA[g2 + 1] - b0;
+                nl[pos + __popc(m & lt_mask)] = make_int4(g2, pair_rank(min(p, q), max(p, q), n_orb), b0, len);
+                work += len > thr_single ? 64 : len;
             }
             pos += __popc(m);
         }
+        for (int o = 16; o; o >>= 1) work += __shfl_xor_sync(0xffffffffu, work, o);
+        if (lane == 0) cost[g] = work;
+    }
+}
+
+// per-row work estimates of the three row kernels (sort keys for a longest-first
+// row order): same-spin list lengths (probes above thr_d), adjacent-alpha work
+__global__ void k_row_cost(TabSpin T, int64_t row_begin, int64_t n_rows, int32_t thr_d, int32_t thr_rowheavy,
+                           const int32_t *nl_cost, uint32_t *c3, uint32_t *c20, uint32_t *c24, int32_t *iota) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = row_begin + r;
+        const int32_t ga = T.ga_of[i], gb = T.gb_of[i];
+        const int32_t la = T.offA[ga + 1] - T.offA[ga], lb = T.offB[gb + 1] - T.offB[gb];
+        c3[r] = (uint32_t)(lb > thr_d ? 4096 : lb);
+        c20[r] = (uint32_t)(la > thr_d ? 4096 : la);
+        c24[r] = la > thr_rowheavy ? 0u : (uint32_t)nl_cost[ga];
+        iota[r] = (int32_t)r;
     }
 }
 
@@ -1619,6 +1641,10 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
             k_csr<<<g, 256, 0, st>>>(k1, perm2, incl, n, t->sa, t->offB, t->gb_of, t->listB_a, t->listB_idx,
                                      nullptr, nullptr, 0);
     }
+    t->thr_single = 192;
+    t->thr_double = 4096;
+    if (const char *e = std::getenv("NNQS_THR_SINGLE")) t->thr_single = std::atoi(e);   // tuning only
+    if (const char *e = std::getenv("NNQS_THR_DOUBLE")) t->thr_double = std::atoi(e);
     // adjacent-alpha lists per alpha group (phase (iii) streams them instead of
     // repeating the 675 alpha-string lookups for every row of the group)
     {
@@ -1626,25 +1652,24 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
         const int n_orb = h->spin.n;
         const int64_t maxc = (int64_t)(n_orb / 2) * (n_orb - n_orb / 2);   // max occupied x empty
         const size_t rb = (8 * (size_t)ng + 15) & ~size_t(15);            // 16-B aligned regions
-        const size_t bytes = rb + 64 + 16 * (size_t)(ng * maxc + 1);
+        const size_t cb = (4 * (size_t)ng + 15) & ~size_t(15);
+        const size_t bytes = rb + 64 + cb + 16 * (size_t)(ng * maxc + 1);
         rc = cuda_check(cudaMallocAsync(&t->nl_buf, bytes, st), "alloc nl");
         if (rc) { cudaFreeAsync(scratch, st); return rc; }
         t->nl_rng = t->nl_buf;
         unsigned long long *cursor = (unsigned long long *)((char *)t->nl_buf + rb);
-        t->nl = (char *)t->nl_buf + rb + 64;
+        t->nl_cost = (int32_t *)((char *)t->nl_buf + rb + 64);
+        t->nl = (char *)t->nl_buf + rb + 64 + cb;
         t->bytes += (int64_t)bytes;
         cudaMemsetAsync(cursor, 0, 8, st);
         TabSpin tv{};
         tv.sa = t->sa; tv.listA_idx = t->listA_idx; tv.offA = t->offA;
         tv.ah_keys = t->ah_keys; tv.ah_vals = t->ah_vals; tv.ah_mask = t->ah_mask;
         const int gw = (int)std::min<int64_t>((ng * 32 + 255) / 256, 148 * 32);
-        k_nl<<<std::max(gw, 1), 256, 0, st>>>(tv, n_orb, ng, (int2 *)t->nl_rng, (int4 *)t->nl, cursor);
+        k_nl<<<std::max(gw, 1), 256, 0, st>>>(tv, n_orb, ng, (int2 *)t->nl_rng, (int4 *)t->nl, cursor,
+                                              t->thr_single, t->nl_cost);
     }
     // deletion multimap for heavy groups (sorted CSR + unique-key hash)
-    t->thr_single = 192;
-    t->thr_double = 4096;
-    if (const char *e = std::getenv("NNQS_THR_SINGLE")) t->thr_single = std::atoi(e);   // tuning only
-    if (const char *e = std::getenv("NNQS_THR_DOUBLE")) t->thr_double = std::atoi(e);
     rc = build_multimap(t, n, st, flags, ctmp, tmp);
     if (rc) { cudaFreeAsync(scratch, st); return rc; }
     t->thr_rowheavy = 16384;
@@ -1685,6 +1710,7 @@ void nnqs_table_release_spin(nnqs_table t) {
     if (t->heavy_groups) cudaFreeAsync(t->heavy_groups, (cudaStream_t)t->stream);
     if (t->nl_buf) cudaFreeAsync(t->nl_buf, (cudaStream_t)t->stream);
     t->nl_rng = nullptr;
+    t->nl_cost = nullptr;
     t->nl = t->nl_buf = nullptr;
     t->heavy_groups = nullptr;
     t->n_heavy = 0;
@@ -1793,6 +1819,40 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
             const char *e = std::getenv("NNQS_MINB");
             minb = e ? std::atoi(e) : 44;
         }
+        // longest-first row orders for the three row kernels (work estimates, one
+        // descending sort each); results do not depend on the order
+        int32_t *perm3 = nullptr, *perm20 = nullptr, *perm24 = nullptr;
+        void *pbuf = nullptr;
+        static int lpt = -1;
+        if (lpt < 0) {
+            const char *e = std::getenv("NNQS_LPT");
+            lpt = e ? std::atoi(e) : 1;
+        }
+        if (lpt && t->nl_cost) {
+            size_t tb = 0;
+            cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                                      (const int32_t *)nullptr, (int32_t *)nullptr, (int)n_rows, 0,
+                                                      32, st);
+            const size_t nb = ((size_t)4 * n_rows + 255) & ~size_t(255);
+            rc = cuda_check(cudaMallocAsync(&pbuf, 8 * nb + tb + 256, st), "alloc row orders");
+            if (rc) return rc;
+            char *pp = (char *)pbuf;
+            uint32_t *c3 = (uint32_t *)pp, *c20 = (uint32_t *)(pp + nb), *c24 = (uint32_t *)(pp + 2 * nb);
+            int32_t *io = (int32_t *)(pp + 3 * nb);
+            perm3 = (int32_t *)(pp + 4 * nb);
+            perm20 = (int32_t *)(pp + 5 * nb);
+            perm24 = (int32_t *)(pp + 6 * nb);
+            uint32_t *ks = (uint32_t *)(pp + 7 * nb);
+            void *tmp = pp + 8 * nb;
+            k_row_cost<<<grid_for(n_rows, 256), 256, 0, st>>>(tv, row_begin, n_rows, t->thr_double, t->thr_rowheavy,
+                                                             t->nl_cost, c3, c20, c24, io);
+            uint32_t *cs[3] = {c3, c20, c24};
+            int32_t *ps[3] = {perm3, perm20, perm24};
+            for (int k = 0; k < 3; ++k) {
+                size_t tb1 = tb;
+                cub::DeviceRadixSort::SortPairsDescending(tmp, tb1, cs[k], ks, io, ps[k], (int)n_rows, 0, 32, st);
+            }
+        }
         static int dyn = -1;
         if (dyn < 0) {
             const char *e = std::getenv("NNQS_DYN");
@@ -1805,7 +1865,7 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
             cudaMemsetAsync(ctr, 0, 64, st);
         }
         int nl = 0;
-        auto launch = [&](auto kern) {
+        auto launch = [&](auto kern, const int32_t *perm) {
             int gg = g;
             if (dyn) {
                 int per_sm = 0;
@@ -1813,24 +1873,26 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
                 gg = std::max(1, per_sm) * 148;
             }
             kern<<<gg, 256, 0, st>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc, (unsigned long long *)stats,
-                                     pairs, phase_mask, acc_heavy, t->thr_rowheavy, partial, ctr ? ctr + nl : nullptr);
+                                     pairs, phase_mask, acc_heavy, t->thr_rowheavy, partial, ctr ? ctr + nl : nullptr,
+                                     ctr ? perm : nullptr);
             ++nl;
         };
         // three launches, each a smaller kernel (instruction cache): diagonal + phase (i)
         // -> partial; phase (ii) adds; phase (iii) adds and finalises
         switch (minb / 10) {
-            case 3: launch(k_eloc_spin<3, 3, false>); launch(k_eloc_spin<20, 3, false>); break;
-            default: launch(k_eloc_spin<3, 4, false>); launch(k_eloc_spin<20, 4, false>);
+            case 3: launch(k_eloc_spin<3, 3, false>, perm3); launch(k_eloc_spin<20, 3, false>, perm20); break;
+            default: launch(k_eloc_spin<3, 4, false>, perm3); launch(k_eloc_spin<20, 4, false>, perm20);
         }
         if (t->n_direct) {
-            launch(k_eloc_spin<3, 4, true>);
-            launch(k_eloc_spin<20, 4, true>);
+            launch(k_eloc_spin<3, 4, true>, perm3);
+            launch(k_eloc_spin<20, 4, true>, perm20);
         }
         switch (minb % 10) {
-            case 3: launch(k_eloc_spin<24, 3, false>); break;
-            default: launch(k_eloc_spin<24, 4, false>);
+            case 3: launch(k_eloc_spin<24, 3, false>, perm24); break;
+            default: launch(k_eloc_spin<24, 4, false>, perm24);
         }
-        if (t->n_direct) launch(k_eloc_spin<24, 4, true>);
+        if (t->n_direct) launch(k_eloc_spin<24, 4, true>, perm24);
+        if (pbuf) cudaFreeAsync(pbuf, st);
         if (ctr) cudaFreeAsync(ctr, st);
         cudaFreeAsync(partial, st);
     }
