@@ -196,6 +196,21 @@ int nnqs_energy_reduce(const double *eloc, const int64_t *counts, int64_t n, dou
                        void *cuda_stream);
 
 /*
+ * Gradient weights of Eq. (7): with
+ * ln Psi* = ln|Psi| - i phi, the estimator 2 Re E_p[(E_loc - E) grad ln Psi*]
+ * over the unique samples with counts w_u is sum_u a_u grad ln|Psi(x_u)| +
+ * b_u grad phi(x_u), where
+ *   a_u = 2 w_u Re(E_loc(x_u) - mean) / W,   b_u = 2 w_u Im(E_loc(x_u) - mean) / W.
+ * eloc device f64[n][2], counts device i64[n], energy_dev device f64[3] =
+ * (mean_re, mean_im, W) -- e.g. nnqs_energy_combine's pass-1 output, global over
+ * all ranks; ab_out device f64[n][2] = (a_u, b_u).  Stream-ordered;
+ * NNQS_E_ARG on bad arguments.  The ansatz backward that consumes the weights
+ * is outside this library.
+ */
+int nnqs_grad_weights(const double *eloc, const int64_t *counts, int64_t n, const double *energy_dev,
+                      double *ab_out, void *cuda_stream);
+
+/*
  * Parity/debug (small inputs): every (row, group) whose x' = x ^ X_k is found
  * in the table, with its index and H_xx'.  rows: host u64[n_rows][2].  Outputs
  * host arrays of capacity max_pairs; n_pairs_out = number found (may exceed

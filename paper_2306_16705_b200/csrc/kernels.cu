@@ -559,6 +559,29 @@ extern "C" int nnqs_energy_combine(const double *partials, int64_t n_chunks, int
     return cuda_check(cudaGetLastError(), "combine launch");
 }
 
+// Eq. (7) weights: a_u = 2 w_u Re(E_u - mean) / W,
+// b_u = 2 w_u Im(E_u - mean) / W; energy = (mean_re, mean_im, W).
+__global__ void k_grad_weights(const double2 *eloc, const int64_t *counts, int64_t n, const double *energy,
+                               double2 *ab) {
+    const double mre = energy[0], mim = energy[1], W = energy[2];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 e = eloc[i];
+        const double f = 2.0 * (double)counts[i] / W;
+        ab[i] = make_double2(f * (e.x - mre), f * (e.y - mim));
+    }
+}
+
+extern "C" int nnqs_grad_weights(const double *eloc, const int64_t *counts, int64_t n, const double *energy_dev,
+                                 double *ab_out, void *cuda_stream) {
+    if (n < 0 || (n > 0 && (!eloc || !counts || !energy_dev || !ab_out)))
+        return nnqs_set_error(NNQS_E_ARG, "nnqs_grad_weights: bad arguments");
+    if (n == 0) return NNQS_OK;
+    k_grad_weights<<<grid_for(n, 256), 256, 0, (cudaStream_t)cuda_stream>>>((const double2 *)eloc, counts, n,
+                                                                          energy_dev, (double2 *)ab_out);
+    return cuda_check(cudaGetLastError(), "grad weights launch");
+}
+
 extern "C" int nnqs_energy_reduce(const double *eloc, const int64_t *counts, int64_t n,
                                   double out[4], void *cuda_stream) {
     if (n <= 0 || !eloc || !counts || !out)

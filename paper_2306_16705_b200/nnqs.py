@@ -38,6 +38,7 @@ _sig = {
     "nnqs_set_algorithm": ([ctypes.c_int], ctypes.c_int),
     "nnqs_get_algorithm": ([], ctypes.c_int),
     "nnqs_debug_counters": ([P, ctypes.c_int], ctypes.c_int),
+    "nnqs_grad_weights": ([P, P, I64, P, P, P], ctypes.c_int),
     "nnqs_energy_chunk_partials": ([P, P, I64, P, P, P], ctypes.c_int),
     "nnqs_energy_combine": ([P, I64, ctypes.c_int, P, P], ctypes.c_int),
     "nnqs_energy_reduce": ([P, P, I64, P, P], ctypes.c_int),
@@ -249,6 +250,17 @@ def nnqs_energy_combine(partials, pass_: int, out_dev=None, n_chunks: int | None
     nc = int(partials.shape[0]) if n_chunks is None else int(n_chunks)
     _check(_lib.nnqs_energy_combine(_dev_ptr(partials), nc, int(pass_), _dev_ptr(out_dev), _stream(stream)))
     return out_dev
+
+
+def nnqs_grad_weights(eloc, counts, energy_dev, ab_out=None, stream=None):
+    """Eq. (7) weights (a_u, b_u) as a device f64[n][2]; energy_dev = (mean_re, mean_im, W, ...)."""
+    import torch
+    n = int(eloc.shape[0])
+    if ab_out is None:
+        ab_out = torch.empty((n, 2), dtype=torch.float64, device=eloc.device)
+    _check(_lib.nnqs_grad_weights(_dev_ptr(eloc), _dev_ptr(counts), n, _dev_ptr(energy_dev), _dev_ptr(ab_out),
+                                  _stream(stream)))
+    return ab_out
 
 
 def nnqs_energy_reduce(eloc, counts, stream=None):

@@ -414,3 +414,22 @@ def test_tiny_amplitude_row_fallback(nnqs, dev):
     got = _c(nnqs.nnqs_local_energy(ham, tab, 0, n_rows=len(st.keys)))
     ref, scale = R.eloc(m.h1, m.h2, m.e_core, st.keys, lp, keys=st.keys, logpsi=lp, with_scale=True)
     _assert_close(got, ref, scale, "tiny psi")
+
+
+def test_grad_weights_matches_oracle(nnqs, dev):
+    """Eq. (7) weights on the GPU (nnqs_grad_weights with the device energy of
+    nnqs_energy_combine) vs the oracle's, on C4 local energies and counts."""
+    st = C.sample_table(4, "full")
+    ham = ham_for(nnqs, 4)
+    tab = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(st.logpsi, dev))
+    n = len(st.keys)
+    el = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n)
+    cnt = _t(st.counts, dev)
+    part = nnqs.nnqs_energy_chunk_partials(el, cnt)
+    m1 = nnqs.nnqs_energy_combine(part, 1)
+    ab = nnqs.nnqs_grad_weights(el, cnt, m1).cpu().numpy()
+    a, b = energy.grad_weights(_c(el), st.counts)
+    W = float(st.counts.sum())
+    tol = 1e-12 * 2 * st.counts * np.abs(_c(el)).max() / W + 1e-300
+    assert np.all(np.abs(ab[:, 0] - a) <= tol) and np.all(np.abs(ab[:, 1] - b) <= tol)
+    assert abs(ab[:, 0].sum()) <= 1e-9 * np.abs(ab[:, 0]).sum()

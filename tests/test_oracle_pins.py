@@ -307,3 +307,48 @@ def test_reduce_spec_examples():
     assert m == 1.0 and v == 3.0 and W == 4
     with pytest.raises(ValueError):
         energy.energy([1.0], [0])
+
+
+# ---------------------------------------------- Eq. (7) gradient weights (NEXT-3)
+@pytest.mark.parametrize("which", ["h2", "n4"])
+def test_grad_weights_equal_finite_differences(which):
+    """Eq. (7): with psi(x) = sqrt(c_x) exp(theta_x + i phi_x)
+    over the whole Fock space (integer weights c_x = |psi|^2 at theta = 0), the
+    weights a_x, b_x of grad ln|psi(x)| and grad phi(x) are exactly dE/dtheta_x and
+    dE/dphi_x of E = <psi|H|psi>/<psi|psi>, H built independently from Kronecker
+    ladder operators -- central differences, relative error <= 1e-6."""
+    if which == "h2":
+        m = C.molecule(1)
+        h1, h2, ec = m.h1, m.h2, m.e_core
+    else:
+        h1, h2, ec = I.synthetic_integrals(4, [0, 1, 0, 1], 77, e_core=3.0)
+    N = 2 * h1.shape[0]
+    dim = 1 << N
+    rng = np.random.default_rng(5)
+    c = rng.integers(1, 10, size=dim)
+    phi = rng.uniform(-np.pi, np.pi, size=dim)
+    H = dense.kron_dense_H(h1, h2, ec)
+
+    def E(theta, ph):
+        psi = np.sqrt(c) * np.exp(theta + 1j * ph)
+        return float(np.real(np.vdot(psi, H @ psi)) / np.real(np.vdot(psi, psi)))
+
+    lp = np.stack([0.5 * np.log(c), phi], axis=1)
+    el = R.eloc(h1, h2, ec, np.array([[x, 0] for x in range(dim)], dtype=np.uint64), lp, keys=None, logpsi=lp)
+    a, b = energy.grad_weights(el, c)
+    eps = 1e-5
+    z = np.zeros(dim)
+    for x in rng.choice(dim, size=min(dim, 12), replace=False):
+        e = np.zeros(dim)
+        e[x] = eps
+        da = (E(z + e, phi) - E(z - e, phi)) / (2 * eps)
+        db = (E(z, phi + e) - E(z, phi - e)) / (2 * eps)
+        scale = max(1e-3, np.max(np.abs(a)), np.max(np.abs(b)))
+        assert abs(da - a[x]) <= 1e-6 * scale, (x, da, a[x])
+        assert abs(db - b[x]) <= 1e-6 * scale, (x, db, b[x])
+
+
+def test_grad_weights_constant_eloc_is_zero():
+    """Constant E_loc gives exactly zero weights (centred estimator)."""
+    a, b = energy.grad_weights(np.full(7, -1.25 + 0.5j), [1, 2, 3, 4, 5, 6, 7])
+    assert np.all(a == 0.0) and np.all(b == 0.0)
