@@ -1106,7 +1106,41 @@ __global__ void k_hj_eval(SpinView S, GroupView G, TabSpin T, const int32_t *hea
             const double2 lx = T.logpsi[e];
             const bool direct = (lx.x - s) < -600.0;
             double ar = 0.0, ai = 0.0;
-            for (int32_t j = hb + lane; j < he; j += 32) {
+            int32_t j = hb + lane;
+            if (kbits && !direct) {
+                // four hits per lane in flight: keys -> (offsets, psi_hat) -> strings;
+                // accumulation order unchanged (j ascending per lane)
+                for (; j + 96 < he; j += 128) {
+                    int32_t kk[4], ix[4];
+                    uint32_t b0[4], b1[4];
+                    double2 ps[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const u64 key = keys[j + 32 * u];
+                        ix[u] = (int32_t)((key >> kbits) & imask);
+                        kk[u] = (int32_t)(key & kmask);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        b0[u] = __ldg(G.goff + kk[u]);
+                        b1[u] = __ldg(G.goff + kk[u] + 1);
+                        ps[u] = __ldg(T.psi_hat + ix[u]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        double hv = 0.0;
+                        for (uint32_t i = b0[u]; i < b1[u]; ++i) {
+                            const ulonglong2 Z = __ldg(G.tz + i);
+                            hv += flip_sign2(__ldg(G.td + i), (__popcll(xk.x & Z.x) + __popcll(xk.y & Z.y)) & 1);
+                        }
+                        c_str += b1[u] - b0[u];
+                        ar = fma(hv, ps[u].x, ar);
+                        ai = fma(hv, ps[u].y, ai);
+                        ++c_hit;
+                    }
+                }
+            }
+            for (; j < he; j += 32) {
                 const u64 key = keys[j];
                 const int32_t idx = (int32_t)((key >> kbits) & imask);
                 int32_t k;
