@@ -1189,13 +1189,16 @@ __global__ void k_hj_eval(SpinView S, GroupView G, TabSpin T, const int32_t *hea
 // Adjacent alpha strings of each alpha group g (a' = a ^ u, u = one occupied ->
 // one empty orbital, a' present in the table), warp per group, in (occupied,
 // empty) order.
-__global__ void k_nl(TabSpin T, int n_orb, int64_t n_groups, int2 *rng, int4 *nl, unsigned long long *cursor,
-                     int32_t thr_single, int32_t *cost) {
-    // pass 1 counts the present a', one atomic reserves the group's block, pass 2
-    // (the same probes, now cache-hot) writes it: one launch, no host round trip.
-    // Block positions depend on scheduling; each group's list (and its order) does not.
+#define NL_WARPS 4
+__global__ void __launch_bounds__(32 * NL_WARPS) k_nl(TabSpin T, int n_orb, int64_t n_groups, int2 *rng, int4 *nl,
+                                                     unsigned long long *cursor, int32_t thr_single, int32_t *cost) {
+    // one pass: the present a' are compacted into the warp's shared buffer, one
+    // atomic reserves the group's block, the buffer is written out.  Block
+    // positions depend on scheduling; each group's list (and its order) does not.
+    __shared__ int2 s_nl[NL_WARPS][1024];          // (g', u rank); occupied x empty <= 1024 for n <= 64
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
+    int2 *buf = s_nl[threadIdx.x >> 5];
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const u64 nmask = n_orb >= 64 ? ~0ULL : ((1ULL << n_orb) - 1);
@@ -1208,17 +1211,6 @@ __global__ void k_nl(TabSpin T, int n_orb, int64_t n_groups, int2 *rng, int4 *nl
         for (int c0 = 0; c0 < combos; c0 += 32) {
             const int c = c0 + lane;
             int32_t g2 = -1;
-            if (c < combos) g2 = alpha_lookup(T, a ^ (1ULL << nth_set(a, c / nva)) ^ (1ULL << nth_set(va, c % nva)));
-            cnt += __popc(__ballot_sync(0xffffffffu, g2 >= 0));
-        }
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(cursor, (unsigned long long)cnt);
-        int32_t pos = (int32_t)__shfl_sync(0xffffffffu, base, 0);
-        if (lane == 0) rng[g] = make_int2(pos, pos + cnt);
-        int32_t work = 0;                            // phase (iii) work estimate of a row of g
-        for (int c0 = 0; c0 < combos; c0 += 32) {
-            const int c = c0 + lane;
-            int32_t g2 = -1;
             int p = 0, q = 0;
             if (c < combos) {
                 p = nth_set(a, c / nva);
@@ -1226,15 +1218,24 @@ __global__ void k_nl(TabSpin T, int n_orb, int64_t n_groups, int2 *rng, int4 *nl
                 g2 = alpha_lookup(T, a ^ (1ULL << p) ^ (1ULL << q));
             }
             const unsigned m = __ballot_sync(0xffffffffu, g2 >= 0);
-            if (g2 >= 0) {
-                const int32_t b0 = T.offA[g2], len = T.offA[g2 + 1] - b0;
-                nl[pos + __popc(m & lt_mask)] = make_int4(g2, pair_rank(min(p, q), max(p, q), n_orb), b0, len);
-                work += len > thr_single ? 64 : len;
-            }
-            pos += __popc(m);
+            if (g2 >= 0) buf[cnt + __popc(m & lt_mask)] = make_int2(g2, pair_rank(min(p, q), max(p, q), n_orb));
+            cnt += __popc(m);
+        }
+        __syncwarp();
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(cursor, (unsigned long long)cnt);
+        const int32_t pos = (int32_t)__shfl_sync(0xffffffffu, base, 0);
+        if (lane == 0) rng[g] = make_int2(pos, pos + cnt);
+        int32_t work = 0;                            // phase (iii) work estimate of a row of g
+        for (int c = lane; c < cnt; c += 32) {
+            const int2 e = buf[c];
+            const int32_t b0 = T.offA[e.x], len = T.offA[e.x + 1] - b0;
+            nl[pos + c] = make_int4(e.x, e.y, b0, len);
+            work += len > thr_single ? 64 : len;
         }
         for (int o = 16; o; o >>= 1) work += __shfl_xor_sync(0xffffffffu, work, o);
         if (lane == 0) cost[g] = work;
+        __syncwarp();
     }
 }
 
@@ -1699,9 +1700,9 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
         TabSpin tv{};
         tv.sa = t->sa; tv.listA_idx = t->listA_idx; tv.offA = t->offA;
         tv.ah_keys = t->ah_keys; tv.ah_vals = t->ah_vals; tv.ah_mask = t->ah_mask;
-        const int gw = (int)std::min<int64_t>((ng * 32 + 255) / 256, 148 * 32);
-        k_nl<<<std::max(gw, 1), 256, 0, st>>>(tv, n_orb, ng, (int2 *)t->nl_rng, (int4 *)t->nl, cursor,
-                                              t->thr_single, t->nl_cost);
+        const int gw = (int)std::min<int64_t>((ng + NL_WARPS - 1) / NL_WARPS, 148 * 48);
+        k_nl<<<std::max(gw, 1), 32 * NL_WARPS, 0, st>>>(tv, n_orb, ng, (int2 *)t->nl_rng, (int4 *)t->nl, cursor,
+                                                        t->thr_single, t->nl_cost);
     }
     // deletion multimap for heavy groups (sorted CSR + unique-key hash)
     rc = build_multimap(t, n, st, flags, ctmp, tmp);
