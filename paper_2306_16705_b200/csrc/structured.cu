@@ -224,6 +224,30 @@ __device__ __forceinline__ int32_t same_spin_tag(const SpinView &S, int spin, u6
 
 // multimap lookup: [beg, end) into mm_ent of the entries stored under (key, meta).
 // A slot is 32 B (one sector): {key, meta | beg << 32}, {end, -}.
+__device__ __forceinline__ bool mm_bloom_pass(const TabSpin &T, u64 h) {
+    const u64 bw = __ldg(T.mm_bloom + ((h >> 32) & T.mm_bloom_mask));
+    return (bw >> ((h >> 20) & 63)) & (bw >> ((h >> 26) & 63)) & 1;
+}
+
+// slot probe of a key that passed the Bloom filter
+__device__ __forceinline__ void mm_find_slots(const TabSpin &T, u64 h, u64 key, uint32_t meta, int32_t &beg,
+                                              int32_t &end) {
+    beg = end = 0;
+    u64 pos = h & T.mm_mask;
+    while (true) {
+        const ulonglong2 v = __ldg(T.mm + 2 * pos);
+        const ulonglong2 w = __ldg(T.mm + 2 * pos + 1);
+        const uint32_t sm = (uint32_t)v.y;
+        if (sm == MM_EMPTY) return;
+        if (v.x == key && sm == meta) {
+            beg = (int32_t)(v.y >> 32);
+            end = (int32_t)w.x;
+            return;
+        }
+        pos = (pos + 1) & T.mm_mask;
+    }
+}
+
 __device__ __forceinline__ void mm_find(const TabSpin &T, u64 key, uint32_t meta, int32_t &beg, int32_t &end) {
     const u64 h = mm_hash(key, meta);
     beg = end = 0;
@@ -403,6 +427,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
     __shared__ int2 s_q[WARPS_PER_BLOCK][QCAP];
     __shared__ uint8_t s_orb[WARPS_PER_BLOCK][4][64];   // occ(a), vir(a), occ(b), vir(b) of the row
     __shared__ int2 s_h[(PH & 8) ? WARPS_PER_BLOCK : 1][HCAP];   // heavy adjacent alpha groups (g, u rank)
+    __shared__ int32_t s_pl[(PH & 8) ? WARPS_PER_BLOCK : 1][64];    // Bloom-passing probe tasks
     __shared__ RowState s_row[WARPS_PER_BLOCK];
     __shared__ uint8_t s_oq[(PH & 1) ? WARPS_PER_BLOCK : 1][128];   // occupied qubits (diagonal)
     __shared__ double2 s_acc[WARPS_PER_BLOCK][32];
@@ -665,22 +690,45 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             (void)nvb;
             int nheavy = 0;                          // warp-uniform
             int2 *hl = s_h[(PH & 8) ? (threadIdx.x >> 5) : 0];
+            int32_t *pl = s_pl[(PH & 8) ? (threadIdx.x >> 5) : 0];
             // heavy alpha groups a' = a ^ u: probe (a', b - e_r) for every occupied beta r,
             // nheavy x nob probes spread over the lanes, matches drained warp-wide
             auto probe_heavy = [&]() {
                 PROF_T(t_hv)
                 __syncwarp();
                 const int ntask = nheavy * nob;
-                for (int t0 = 0; t0 < ntask; t0 += 32) {
-                    const int t = t0 + lane;
+                // Bloom words first; the probes that pass (~25 %) are compacted (task ids)
+                // and only they run the dependent slot -> record -> group chain, 32 at a time
+                int np = 0;
+                for (int t0 = 0; t0 < ntask || np > 0; t0 += 32) {
+                    if (t0 < ntask) {
+                        const int t = t0 + lane;
+                        bool pass = false;
+                        if (t < ntask) {
+                            const int h = t / nob, rr = t - h * nob;
+                            pass = mm_bloom_pass(T, mm_hash(b ^ (1ULL << occB[rr]), mm_meta(0, hl[h].x)));
+                            ++c_cand;
+                        }
+                        const unsigned pm = __ballot_sync(0xffffffffu, pass);
+                        if (pass) pl[np + __popc(pm & lt_mask)] = t;
+                        np += __popc(pm);
+                        if (np < 32 && t0 + 32 < ntask) continue;
+                    }
+                    const int cnt = min(np, 32);
+                    __syncwarp();
                     int32_t mb = 0, me = 0, ur = 0;
-                    if (t < ntask) {
+                    if (lane < cnt) {
+                        const int t = pl[lane];
                         const int h = t / nob, rr = t - h * nob;
                         const int2 hv = hl[h];
                         ur = hv.y;
-                        mm_find(T, b ^ (1ULL << occB[rr]), mm_meta(0, hv.x), mb, me);
-                        ++c_cand;
+                        const u64 key = b ^ (1ULL << occB[rr]);
+                        const uint32_t meta = mm_meta(0, hv.x);
+                        mm_find_slots(T, mm_hash(key, meta), key, meta, mb, me);
                     }
+                    __syncwarp();
+                    if (lane < np - cnt) pl[lane] = pl[lane + cnt];
+                    np -= cnt;
                     drain(mb, me, ur, [&](int32_t mj, int32_t sur, int32_t &k, int32_t &idx) {
                         const ulonglong2 en = __ldg(T.mm_ent + mj);
                         idx = (int32_t)en.y;
