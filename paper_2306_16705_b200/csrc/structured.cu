@@ -614,7 +614,6 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                     for (int u = 0; u < 4; ++u) {
                         const int32_t j = j0 + 32 * u + lane;
                         v[u] = j < je ? __ldg(lst + j) : mine;
-                        ix[u] = j < je ? __ldg(lidx + j) : 0;
                     }
                     int32_t kk[4];
 #pragma unroll
@@ -623,7 +622,11 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         const u64 d = mine ^ v[u];
                         const int c = __popcll(d);
                         kk[u] = -1;
-                        if ((c == 2 || c == 4) && 2 * __popcll(mine & d) == c) kk[u] = same_spin_tag(S, ph, d, c);
+                        ix[u] = 0;
+                        if ((c == 2 || c == 4) && 2 * __popcll(mine & d) == c) {
+                            kk[u] = same_spin_tag(S, ph, d, c);
+                            ix[u] = __ldg(lidx + j);
+                        }
                         c_cand += j < je;
                     }
                     push4(kk, ix);
@@ -789,17 +792,18 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         ur[u] = __shfl_sync(0xffffffffu, urank, lo);
                         jj[u] = ob + (f - oe);
                         v[u] = f < total ? __ldg(T.listA_b + jj[u]) : b;
-                        ix[u] = f < total ? __ldg(T.listA_idx + jj[u]) : 0;   // issued with v: no dependent load on a hit
                     }
                     int32_t kk[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {           // group-id loads of all four issued before any push
-                        const u64 d = b ^ v[u];
+                    for (int u = 0; u < 4; ++u) {           // group-id and index loads of all four issued
+                        const u64 d = b ^ v[u];             // before any push (candidates passing the test)
                         kk[u] = -1;
+                        ix[u] = 0;
                         if (__popcll(d) == 2 && __popcll(b & d) == 1) {
                             const int r1 = __ffsll((long long)d) - 1;
                             const int r2 = 63 - __clzll((long long)d);
                             kk[u] = __ldg(S.ab_k + (int64_t)ur[u] * S.P + pair_rank(r1, r2, S.n));
+                            ix[u] = __ldg(T.listA_idx + jj[u]);
                         }
                         c_cand += (f0 + 32 * u + lane) < total;
                     }
