@@ -92,9 +92,8 @@ struct DeviceHam {
     int32_t *ab_k = nullptr;
     double *diag_uv = nullptr; // diagonal group in occupation form (structured path)
     double *occ_rec = nullptr; // single-excitation groups in occupation form
-    uint32_t *foff = nullptr;  // folded table (structured path)
-    void *fz = nullptr;
-    double *fd = nullptr;
+    void *frng = nullptr;      // folded table (structured path): uint2 range per group,
+    void *frec = nullptr;      // 32-B {Z lo, Z hi, d, 0} per string
     int64_t bytes = 0;
 };
 

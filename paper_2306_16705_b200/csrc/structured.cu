@@ -85,11 +85,17 @@ struct SpinView {
     const double *diag_uv;    // nullptr: evaluate its Pauli strings
 };
 
+// folded table on the device: per group its string range, per string one 32-B
+// record {Z lo, Z hi}, {d bits, 0} (one sector per string instead of two)
 struct GroupView {
-    const uint32_t *goff;
-    const ulonglong2 *tz;
-    const double *td;
+    const uint2 *grng;
+    const ulonglong2 *rec;
 };
+__device__ __forceinline__ uint2 g_range(const GroupView &G, int32_t k) { return __ldg(G.grng + k); }
+__device__ __forceinline__ ulonglong2 g_z(const GroupView &G, uint32_t i) { return __ldg(G.rec + 2 * i); }
+__device__ __forceinline__ double g_d(const GroupView &G, uint32_t i) {
+    return __longlong_as_double((long long)__ldg(G.rec + 2 * i + 1).x);
+}
 
 struct TabSpin {
     int64_t n;
@@ -143,12 +149,13 @@ __device__ __forceinline__ double flip_sign2(double d, int parity) {
 // H_{x', x} = sum_{i in group k} d_i (-1)^{popc(x & Z_i)}  (one lane)
 __device__ __forceinline__ double group_value1(const GroupView &G, int32_t k, u64 x0, u64 x1,
                                                unsigned long long &n_str) {
-    const uint32_t b = __ldg(G.goff + k), e = __ldg(G.goff + k + 1);
+    const uint2 be = g_range(G, k);
+    const uint32_t b = be.x, e = be.y;
     double hv = 0.0;
 #pragma unroll 4
     for (uint32_t i = b; i < e; ++i) {
-        const ulonglong2 Z = __ldg(G.tz + i);
-        hv += flip_sign2(__ldg(G.td + i), (__popcll(x0 & Z.x) + __popcll(x1 & Z.y)) & 1);
+        const ulonglong2 Z = g_z(G, i);
+        hv += flip_sign2(g_d(G, i), (__popcll(x0 & Z.x) + __popcll(x1 & Z.y)) & 1);
     }
     n_str += e - b;
     return hv;
@@ -166,8 +173,8 @@ __device__ __forceinline__ double warp_strided_sum(const GroupView &G, uint32_t 
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const bool ok = t0 + 32 * u < e;
-            Z[u] = ok ? __ldg(G.tz + t0 + 32 * u) : make_ulonglong2(0, 0);
-            d[u] = ok ? __ldg(G.td + t0 + 32 * u) : 0.0;
+            Z[u] = ok ? g_z(G, t0 + 32 * u) : make_ulonglong2(0, 0);
+            d[u] = ok ? g_d(G, t0 + 32 * u) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -316,8 +323,9 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
         e = q[(qh + lane) & (QCAP - 1)];          // ring buffer: no shifting after a flush
         occ = OCC && e.x < 0;                      // single excitation, occupation-form record
         if (!occ) {
-            gb0 = __ldg(G.goff + e.x);
-            ge0 = __ldg(G.goff + e.x + 1);
+            const uint2 be = g_range(G, e.x);
+            gb0 = be.x;
+            ge0 = be.y;
         }
         if (!direct) ps0 = __ldg(psi_hat + e.y);   // issued with the offsets, used after the sum
         ++c_hit;
@@ -360,8 +368,8 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const bool ok = i0 + u < ge0;
-                Z[u] = ok ? __ldg(G.tz + i0 + u) : make_ulonglong2(0, 0);
-                d[u] = ok ? __ldg(G.td + i0 + u) : 0.0;
+                Z[u] = ok ? g_z(G, i0 + u) : make_ulonglong2(0, 0);
+                d[u] = ok ? g_d(G, i0 + u) : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u)
@@ -577,8 +585,9 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                 ge = (uint32_t)(nocc + nocc * (nocc - 1) / 2);
                 __syncwarp();
             } else {
-                gb = __ldg(G.goff + S.diag_k);
-                ge = __ldg(G.goff + S.diag_k + 1);
+                const uint2 be = g_range(G, S.diag_k);
+                gb = be.x;
+                ge = be.y;
                 hv = warp_strided_sum(G, gb, ge, rs->x0, rs->x1);
             }
             if (lane == 0) {   // x' = x: psi_hat(x) (or 1 on the direct path)
@@ -1174,16 +1183,17 @@ __global__ void k_hj_eval(SpinView S, GroupView G, TabSpin T, const int32_t *hea
                     }
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        b0[u] = __ldg(G.goff + kk[u]);
-                        b1[u] = __ldg(G.goff + kk[u] + 1);
+                        const uint2 be = g_range(G, kk[u]);
+                        b0[u] = be.x;
+                        b1[u] = be.y;
                         ps[u] = __ldg(T.psi_hat + ix[u]);
                     }
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         double hv = 0.0;
                         for (uint32_t i = b0[u]; i < b1[u]; ++i) {
-                            const ulonglong2 Z = __ldg(G.tz + i);
-                            hv += flip_sign2(__ldg(G.td + i), (__popcll(xk.x & Z.x) + __popcll(xk.y & Z.y)) & 1);
+                            const ulonglong2 Z = g_z(G, i);
+                            hv += flip_sign2(g_d(G, i), (__popcll(xk.x & Z.x) + __popcll(xk.y & Z.y)) & 1);
                         }
                         c_str += b1[u] - b0[u];
                         ar = fma(hv, ps[u].x, ar);
@@ -1511,16 +1521,26 @@ int nnqs_spin_index_upload(nnqs_ham h) {
         if ((rc = cuda_check(cudaMemcpy(D.diag_uv, S.diag_uv.data(), bu, cudaMemcpyHostToDevice), "copy diag"))) return rc;
         D.bytes += (int64_t)bu;
     }
-    const size_t bo = 4 * S.foff.size(), bz = 8 * std::max<size_t>(S.fz.size(), 2), bd = 8 * std::max<size_t>(S.fd.size(), 1);
-    if ((rc = cuda_check(cudaMalloc((void **)&D.foff, bo), "alloc foff"))) return rc;
-    if ((rc = cuda_check(cudaMalloc((void **)&D.fz, bz), "alloc fz"))) return rc;
-    if ((rc = cuda_check(cudaMalloc((void **)&D.fd, bd), "alloc fd"))) return rc;
-    if ((rc = cuda_check(cudaMemcpy(D.foff, S.foff.data(), bo, cudaMemcpyHostToDevice), "copy foff"))) return rc;
-    if (!S.fd.empty()) {
-        if ((rc = cuda_check(cudaMemcpy(D.fz, S.fz.data(), 8 * S.fz.size(), cudaMemcpyHostToDevice), "copy fz"))) return rc;
-        if ((rc = cuda_check(cudaMemcpy(D.fd, S.fd.data(), 8 * S.fd.size(), cudaMemcpyHostToDevice), "copy fd"))) return rc;
+    {
+        const int64_t K = (int64_t)S.foff.size() - 1, M = (int64_t)S.fd.size();
+        std::vector<uint32_t> rng(2 * std::max<int64_t>(K, 1), 0);
+        for (int64_t k = 0; k < K; ++k) {
+            rng[2 * k] = S.foff[k];
+            rng[2 * k + 1] = S.foff[k + 1];
+        }
+        std::vector<u64> rec(4 * std::max<int64_t>(M, 1), 0);
+        for (int64_t i = 0; i < M; ++i) {
+            rec[4 * i] = S.fz[2 * i];
+            rec[4 * i + 1] = S.fz[2 * i + 1];
+            std::memcpy(&rec[4 * i + 2], &S.fd[i], 8);
+        }
+        const size_t br = 4 * rng.size(), bq = 8 * rec.size();
+        if ((rc = cuda_check(cudaMalloc((void **)&D.frng, br), "alloc folded ranges"))) return rc;
+        if ((rc = cuda_check(cudaMalloc((void **)&D.frec, bq), "alloc folded strings"))) return rc;
+        if ((rc = cuda_check(cudaMemcpy(D.frng, rng.data(), br, cudaMemcpyHostToDevice), "copy folded ranges"))) return rc;
+        if ((rc = cuda_check(cudaMemcpy(D.frec, rec.data(), bq, cudaMemcpyHostToDevice), "copy folded strings"))) return rc;
+        D.bytes += (int64_t)(br + bq);
     }
-    D.bytes += (int64_t)(bo + bz + bd);
     return NNQS_OK;
 }
 
@@ -1537,12 +1557,10 @@ void nnqs_spin_index_release(nnqs_ham h) {
     D.diag_uv = nullptr;
     cudaFree(D.occ_rec);
     D.occ_rec = nullptr;
-    cudaFree(D.foff);
-    cudaFree(D.fz);
-    cudaFree(D.fd);
-    D.foff = nullptr;
-    D.fz = nullptr;
-    D.fd = nullptr;
+    cudaFree(D.frng);
+    cudaFree(D.frec);
+    D.frng = nullptr;
+    D.frec = nullptr;
 }
 
 namespace {
@@ -1812,7 +1830,7 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
     const DeviceHam &D = h->dev;
     SpinView sv{S.n, S.P, D.pair_k[0], D.pair_k[1], D.quad_k[0], D.quad_k[1], D.ab_k, S.diag_k,
                 h->host.n_qubits, S.occ_ok ? D.occ_rec : nullptr, S.diag_K, S.diag_ok ? D.diag_uv : nullptr};
-    GroupView gv{D.foff, (const ulonglong2 *)D.fz, D.fd};   // in-sector folded strings
+    GroupView gv{(const uint2 *)D.frng, (const ulonglong2 *)D.frec};   // in-sector folded strings
     TabSpin tv{t->n, (const ulonglong2 *)t->keys, (const double2 *)t->logpsi, (const double2 *)t->psi_hat,
                t->slots, t->bucket_mask, t->shift_key, t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB,
                t->listA_b, t->listB_a, t->listA_idx, t->listB_idx, t->ah_keys, t->ah_vals, t->ah_mask,
