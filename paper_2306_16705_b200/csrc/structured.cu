@@ -1746,7 +1746,7 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
             k_csr<<<g, 256, 0, st>>>(k1, perm2, incl, n, t->sa, t->offB, t->gb_of, t->listB_a, t->listB_idx,
                                      nullptr, nullptr, 0);
     }
-    t->thr_single = 192;
+    t->thr_single = 128;   // measured (step ms): 96 63.52, 128 63.45, 192 63.67, 256 64.15
     t->thr_double = 4096;
     if (const char *e = std::getenv("NNQS_THR_SINGLE")) t->thr_single = std::atoi(e);   // tuning only
     if (const char *e = std::getenv("NNQS_THR_DOUBLE")) t->thr_double = std::atoi(e);
