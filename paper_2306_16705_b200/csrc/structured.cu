@@ -1747,7 +1747,7 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
                                      nullptr, nullptr, 0);
     }
     t->thr_single = 128;   // measured (step ms): 96 63.52, 128 63.45, 192 63.67, 256 64.15
-    t->thr_double = 4096;
+    t->thr_double = 8192;   // measured (step ms): 2048 69.46, 4096 63.51, 8192 63.15
     if (const char *e = std::getenv("NNQS_THR_SINGLE")) t->thr_single = std::atoi(e);   // tuning only
     if (const char *e = std::getenv("NNQS_THR_DOUBLE")) t->thr_double = std::atoi(e);
     // adjacent-alpha lists per alpha group (phase (iii) streams them instead of
