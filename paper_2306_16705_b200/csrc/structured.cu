@@ -953,34 +953,78 @@ __global__ void k_mm_count(const u64 *sa, const u64 *sb, const int32_t *ga_of, c
     }
 }
 
-// emit (key, meta, entry) at the entry's exclusive-scan offset (deterministic order)
-__global__ void k_mm_emit(const u64 *sa, const u64 *sb, const int32_t *ga_of, const int32_t *gb_of,
-                          const int32_t *offA, const int32_t *offB, int64_t n, int32_t thr_s, int32_t thr_d,
-                          const int64_t *eoff, u64 *K, uint32_t *M, int32_t *V, u64 *SV) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-         e += (int64_t)gridDim.x * blockDim.x) {
+// Balanced emission: block of 256 entries, their keys (up to 15 + 105 + 15 + 105
+// each) flattened through a block prefix sum and written by all threads, coalesced.
+// Same key set and the same entry order per run as k_mm_emit (a run's entries are
+// ordered by entry index; each entry contributes at most one key to a run).
+__global__ void __launch_bounds__(256) k_mm_emit_flat(const u64 *sa, const u64 *sb, const int32_t *ga_of,
+                                                      const int32_t *gb_of, const int32_t *offA, const int32_t *offB,
+                                                      int64_t n, int32_t thr_s, int32_t thr_d, const int32_t *counts,
+                                                      const int64_t *eoff, u64 *K, uint32_t *M, int32_t *V,
+                                                      u64 *SV) {
+    typedef cub::BlockScan<int32_t, 256> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int32_t s_pre[257];
+    __shared__ u64 s_a[256], s_b[256];
+    __shared__ int32_t s_ga[256], s_gb[256];
+    __shared__ uint8_t s_f[256];
+    const int64_t e0 = (int64_t)blockIdx.x * 256;
+    const int64_t e = e0 + threadIdx.x;
+    int32_t c = 0;
+    if (e < n) {
+        c = counts[e];
         const int32_t ga = ga_of[e], gb = gb_of[e];
         const int32_t la = offA[ga + 1] - offA[ga], lb = offB[gb + 1] - offB[gb];
-        int64_t o = eoff[e];
-        for (int side = 0; side < 2; ++side) {
-            const int32_t len = side == 0 ? la : lb;   // side 0: beta deletions keyed by alpha group
-            const u64 w = side == 0 ? sb[e] : sa[e];
-            const int32_t g = side == 0 ? ga : gb;
-            const int tag = side == 0 ? 0 : 2;
-            if (len <= (side == 0 ? thr_s : thr_d)) continue;   // alpha groups: also phase (iii) neighbours
-            for (u64 m1 = w; m1; m1 &= m1 - 1) {
-                const u64 b1 = m1 & (~m1 + 1);
-                K[o] = w ^ b1; M[o] = mm_meta(tag, g); V[o] = (int32_t)e; SV[o] = w; ++o;
-            }
-            if (len > thr_d)
-                for (u64 m1 = w; m1; m1 &= m1 - 1) {
-                    const u64 b1 = m1 & (~m1 + 1);
-                    for (u64 m2 = m1 & (m1 - 1); m2; m2 &= m2 - 1) {
-                        const u64 b2 = m2 & (~m2 + 1);
-                        K[o] = w ^ b1 ^ b2; M[o] = mm_meta(tag + 1, g); V[o] = (int32_t)e; SV[o] = w; ++o;
-                    }
-                }
+        s_a[threadIdx.x] = sa[e];
+        s_b[threadIdx.x] = sb[e];
+        s_ga[threadIdx.x] = ga;
+        s_gb[threadIdx.x] = gb;
+        s_f[threadIdx.x] = (uint8_t)((la > thr_s ? 1 : 0) | (la > thr_d ? 2 : 0) | (lb > thr_d ? 12 : 0));
+    }
+    int32_t ex, total;
+    Scan(tmp).ExclusiveSum(c, ex, total);
+    s_pre[threadIdx.x] = ex;
+    if (threadIdx.x == 0) s_pre[256] = total;
+    __syncthreads();
+    if (e0 >= n) return;
+    const int64_t base = eoff[e0];
+    for (int32_t p = threadIdx.x; p < total; p += 256) {
+        int lo = 0, hi = 256;                          // last t with s_pre[t] <= p
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_pre[mid] <= p) lo = mid; else hi = mid;
         }
+        int32_t l = p - s_pre[lo];
+        const uint8_t f = s_f[lo];
+        u64 key = 0, w = 0;
+        uint32_t meta = 0;
+        for (int side = 0; side < 2; ++side) {
+            const u64 ws = side == 0 ? s_b[lo] : s_a[lo];      // side 0: beta deletions keyed by the alpha group
+            const int32_t gs = side == 0 ? s_ga[lo] : s_gb[lo];
+            const int tag = side == 0 ? 0 : 2;
+            const int ns = __popcll(ws);
+            if (f & (side == 0 ? 1 : 4)) {
+                if (l < ns) { key = ws ^ (1ULL << nth_set(ws, l)); meta = mm_meta(tag, gs); w = ws; break; }
+                l -= ns;
+            }
+            if (f & (side == 0 ? 2 : 8)) {
+                const int np = ns * (ns - 1) / 2;
+                if (l < np) {
+                    int i1, i2;
+                    nth_pair(l, i1, i2);
+                    key = ws ^ (1ULL << nth_set(ws, i1)) ^ (1ULL << nth_set(ws, i2));
+                    meta = mm_meta(tag + 1, gs);
+                    w = ws;
+                    break;
+                }
+                l -= np;
+            }
+        }
+        const int64_t o = base + p;
+        K[o] = key;
+        M[o] = meta;
+        V[o] = (int32_t)(e0 + lo);
+        SV[o] = w;
     }
 }
 
@@ -1625,8 +1669,9 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
             *P2 = (int32_t *)take(4 * m);
     void *ct = take(ctb);
     const int gm = grid_for(m, 256);
-    k_mm_emit<<<g, 256, 0, st>>>(t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB, n, t->thr_single,
-                                 t->thr_double, eoff, K, M, V, SV);
+    k_mm_emit_flat<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB,
+                                                               n, t->thr_single, t->thr_double, counts, eoff, K, M,
+                                                               V, SV);
     k_iota<<<gm, 256, 0, st>>>(io, m);
     size_t tb1 = ctb;
     cub::DeviceRadixSort::SortPairs(ct, tb1, K, K1, io, P1, (int)m, 0, 64, st);
