@@ -143,6 +143,7 @@ struct nnqs_table_s {
     int32_t thr_rowheavy = 0;                  // alpha groups with more rows: entry-driven phase (iii)
     int32_t *heavy_groups = nullptr;           // [n_heavy] those alpha group ids (device)
     int64_t n_alpha_groups = 0;
+    int spin_n = 0;                            // spatial orbitals (the Hamiltonian's SpinIndex::n)
     void *nl_rng = nullptr;                    // int2 [n_alpha_groups]: adjacent-alpha list range (structured.cu k_nl)
     void *nl = nullptr;                        // int4 {g', u rank, offA[g'], len}
     int32_t *nl_cost = nullptr;                // [n_alpha_groups] phase (iii) work estimate of a row

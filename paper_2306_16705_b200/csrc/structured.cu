@@ -46,6 +46,8 @@ int ensure_hs(int device) {
     return NNQS_OK;
 }
 
+int ensure_binom(int device);
+
 inline int cuda_check(cudaError_t e, const char *what) {
     if (e == cudaSuccess) return NNQS_OK;
     return nnqs_set_error(e == cudaErrorMemoryAllocation ? NNQS_E_NOMEM : NNQS_E_CUDA,
@@ -944,13 +946,47 @@ __device__ __forceinline__ int mm_keys_of(int32_t la, int32_t lb, int na, int nb
 
 __global__ void k_mm_count(const u64 *sa, const u64 *sb, const int32_t *ga_of, const int32_t *gb_of,
                            const int32_t *offA, const int32_t *offB, int64_t n, int32_t thr_s, int32_t thr_d,
-                           int32_t *counts) {
+                           int32_t *counts, int *pc_range, int32_t *flagB) {
+    // also: popcount range of the alpha / beta strings (min a, max a, min b, max b) and
+    // the beta groups that receive keys (for the compact sort key)
+    int mna = 64, mxa = 0, mnb = 64, mxb = 0;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int32_t la = offA[ga_of[e] + 1] - offA[ga_of[e]];
         const int32_t lb = offB[gb_of[e] + 1] - offB[gb_of[e]];
-        counts[e] = mm_keys_of(la, lb, __popcll(sa[e]), __popcll(sb[e]), thr_s, thr_d);
+        const int pa = __popcll(sa[e]), pb = __popcll(sb[e]);
+        counts[e] = mm_keys_of(la, lb, pa, pb, thr_s, thr_d);
+        if (lb > thr_d) flagB[gb_of[e]] = 1;
+        mna = min(mna, pa); mxa = max(mxa, pa);
+        mnb = min(mnb, pb); mxb = max(mxb, pb);
     }
+    atomicMin(pc_range + 0, mna);
+    atomicMax(pc_range + 1, mxa);
+    atomicMin(pc_range + 2, mnb);
+    atomicMax(pc_range + 3, mxb);
+}
+
+__global__ void k_flag_alpha(const int32_t *offA, int64_t ng, int32_t thr_s, int32_t *flagA) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng;
+         g += (int64_t)gridDim.x * blockDim.x)
+        flagA[g] = offA[g + 1] - offA[g] > thr_s ? 1 : 0;
+}
+
+// binomials C(p, k), p < 64, k < 32 (colex rank of a deletion string)
+__device__ u64 d_binom[64 * 32];
+
+// Compact sort key of a multimap record: (meta rank << rbits) | colex rank of the key
+// among strings of its popcount -- injective when every alpha (beta) string of the
+// table has one popcount, so one radix sort on ~55 bits groups the runs.
+__device__ __forceinline__ u64 mm_sort_key(u64 key, uint32_t meta, const int32_t *rankA, const int32_t *rankB,
+                                           int32_t NA, int32_t NB, int rbits) {
+    const int tag = (int)(meta >> 30);
+    const int32_t g = (int32_t)(meta & 0x3FFFFFFFu);
+    const u64 mr = tag < 2 ? (u64)(rankA[g] + (tag == 1 ? NA : 0)) : (u64)(2 * NA + rankB[g] + (tag == 3 ? NB : 0));
+    u64 r = 0;
+    int i = 0;
+    for (u64 w = key; w; w &= w - 1, ++i) r += d_binom[(__ffsll((long long)w) - 1) * 32 + i + 1];
+    return (mr << rbits) | r;
 }
 
 // Balanced emission: block of 256 entries, their keys (up to 15 + 105 + 15 + 105
@@ -961,7 +997,8 @@ __global__ void __launch_bounds__(256) k_mm_emit_flat(const u64 *sa, const u64 *
                                                       const int32_t *gb_of, const int32_t *offA, const int32_t *offB,
                                                       int64_t n, int32_t thr_s, int32_t thr_d, const int32_t *counts,
                                                       const int64_t *eoff, u64 *K, uint32_t *M, int32_t *V,
-                                                      u64 *SV) {
+                                                      u64 *SV, u64 *SK, const int32_t *rankA, const int32_t *rankB,
+                                                      int32_t NA, int32_t NB, int rbits) {
     typedef cub::BlockScan<int32_t, 256> Scan;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ int32_t s_pre[257];
@@ -1025,6 +1062,7 @@ __global__ void __launch_bounds__(256) k_mm_emit_flat(const u64 *sa, const u64 *
         M[o] = meta;
         V[o] = (int32_t)(e0 + lo);
         SV[o] = w;
+        if (SK) SK[o] = mm_sort_key(key, meta, rankA, rankB, NA, NB, rbits);
     }
 }
 
@@ -1608,13 +1646,55 @@ void nnqs_spin_index_release(nnqs_ham h) {
 }
 
 namespace {
+int ensure_binom(int device) {
+    static bool ready[64] = {false};
+    if (device < 0 || device >= 64) return NNQS_E_ARG;
+    if (ready[device]) return NNQS_OK;
+    static u64 tab[64 * 32];
+    for (int p = 0; p < 64; ++p)
+        for (int k = 0; k < 32; ++k) {
+            long double r = (k > p) ? 0.0L : 1.0L;
+            for (int i = 1; i <= k && k <= p; ++i) r = r * (p - k + i) / i;
+            tab[p * 32 + k] = (u64)(r + 0.5L);
+        }
+    cudaError_t e = cudaMemcpyToSymbol(d_binom, tab, sizeof(tab));
+    if (e != cudaSuccess) return nnqs_set_error(NNQS_E_CUDA, cudaGetErrorString(e));
+    ready[device] = true;
+    return NNQS_OK;
+}
+
 int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, void *, size_t) {
     const int g = grid_for(n, 256);
     int64_t *eoff = nullptr;
     int rc = cuda_check(cudaMallocAsync((void **)&eoff, 8 * (n + 1), st), "alloc mm offsets");
     if (rc) return rc;
+    // compact-key support: popcount range, dense ranks of the groups that receive keys
+    const int64_t nga = t->n_alpha_groups;
+    int32_t *rk = nullptr;                       // [pc_range 4 | flagA nga+1 | rankA | flagB n+1 | rankB]
+    rc = cuda_check(cudaMallocAsync((void **)&rk, 4 * (4 + 2 * (nga + 1) + 2 * (n + 1)) + 64, st), "alloc mm ranks");
+    if (rc) { cudaFreeAsync(eoff, st); return rc; }
+    int *pcr = rk;
+    int32_t *flagA = rk + 4, *rankA = flagA + nga + 1, *flagB = rankA + nga + 1, *rankB = flagB + n + 1;
+    {
+        const int init[4] = {64, 0, 64, 0};
+        cudaMemcpyAsync(pcr, init, sizeof(init), cudaMemcpyHostToDevice, st);
+        cudaMemsetAsync(flagB, 0, 4 * (n + 1), st);
+        cudaMemsetAsync(flagA + nga, 0, 4, st);
+    }
     k_mm_count<<<g, 256, 0, st>>>(t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB, n, t->thr_single,
-                                  t->thr_double, counts);
+                                  t->thr_double, counts, pcr, flagB);
+    k_flag_alpha<<<grid_for(nga, 256), 256, 0, st>>>(t->offA, nga, t->thr_single, flagA);
+    {
+        size_t ts1 = 0, ts2 = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, ts1, flagA, rankA, (int)nga + 1, st);
+        cub::DeviceScan::ExclusiveSum(nullptr, ts2, flagB, rankB, (int)n + 1, st);
+        void *tsc = nullptr;
+        rc = cuda_check(cudaMallocAsync(&tsc, std::max(ts1, ts2), st), "alloc rank scan");
+        if (rc) { cudaFreeAsync(rk, st); cudaFreeAsync(eoff, st); return rc; }
+        cub::DeviceScan::ExclusiveSum(tsc, ts1, flagA, rankA, (int)nga + 1, st);
+        cub::DeviceScan::ExclusiveSum(tsc, ts2, flagB, rankB, (int)n + 1, st);
+        cudaFreeAsync(tsc, st);
+    }
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, eoff, (int)n + 1, st);
     void *stmp = nullptr;
@@ -1628,11 +1708,35 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
     cudaMemsetAsync(cz + n, 0, 4, st);
     cub::DeviceScan::ExclusiveSum(stmp, tb, cz, eoff, (int)n + 1, st);
     int64_t m = 0;
+    int hpc[4] = {0, 0, 0, 0};
+    int32_t NA = 0, NB = 0;
     rc = cuda_check(cudaMemcpyAsync(&m, eoff + n, 8, cudaMemcpyDeviceToHost, st), "read mm size");
+    if (!rc) rc = cuda_check(cudaMemcpyAsync(hpc, pcr, sizeof(hpc), cudaMemcpyDeviceToHost, st), "read pc range");
+    if (!rc) rc = cuda_check(cudaMemcpyAsync(&NA, rankA + nga, 4, cudaMemcpyDeviceToHost, st), "read NA");
+    if (!rc) rc = cuda_check(cudaMemcpyAsync(&NB, rankB + n, 4, cudaMemcpyDeviceToHost, st), "read NB");
     if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
     cudaFreeAsync(stmp, st);
     cudaFreeAsync(cz, st);
+    // compact key: one popcount per side, meta rank and colex rank in <= 64 bits
+    int rbits = 0, kbits_all = 65;
+    if (!rc && hpc[0] == hpc[1] && hpc[2] == hpc[3] && t->spin_n <= 64) {
+        auto binom = [](int nn, int kk) -> long double {
+            if (kk < 0 || kk > nn) return 0.0L;
+            long double r = 1.0L;
+            for (int i = 1; i <= kk; ++i) r = r * (nn - kk + i) / i;
+            return r;
+        };
+        long double mx = 1.0L;
+        for (int pc : {hpc[0], hpc[2]})
+            for (int d = 1; d <= 2; ++d) mx = std::max(mx, binom(t->spin_n, pc - d));
+        while (rbits < 64 && (long double)(1ULL << rbits) < mx) ++rbits;
+        int mbits = 0;
+        while ((1LL << mbits) < 2LL * NA + 2LL * NB + 1) ++mbits;
+        kbits_all = rbits + mbits;
+    }
+    const bool compact = kbits_all <= 64 && ensure_binom(t->device) == NNQS_OK;
     if (rc || m == 0) {
+        cudaFreeAsync(rk, st);
         cudaFreeAsync(eoff, st);
         if (!rc) {   // empty multimap: one empty slot
             rc = cuda_check(cudaMallocAsync(&t->mm_buf, 128, st), "alloc mm");
@@ -1647,7 +1751,11 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
         }
         return rc;
     }
-    if (m >= (1LL << 31)) { cudaFreeAsync(eoff, st); return nnqs_set_error(NNQS_E_SIZE, "multimap too large"); }
+    if (m >= (1LL << 31)) {
+        cudaFreeAsync(rk, st);
+        cudaFreeAsync(eoff, st);
+        return nnqs_set_error(NNQS_E_SIZE, "multimap too large");
+    }
     // scratch for the sort
     auto r16 = [](size_t b) { return (b + 15) & ~size_t(15); };
     size_t t1 = 0, t2 = 0, t3 = 0;
@@ -1660,7 +1768,7 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
     const size_t sbytes = 4 * r16(8 * m) + 3 * r16(4 * m) + 4 * r16(4 * m) + r16(ctb) + 64;
     char *sc = nullptr;
     rc = cuda_check(cudaMallocAsync((void **)&sc, sbytes, st), "alloc mm scratch");
-    if (rc) { cudaFreeAsync(eoff, st); return rc; }
+    if (rc) { cudaFreeAsync(rk, st); cudaFreeAsync(eoff, st); return rc; }
     char *sp = sc;
     auto take = [&](size_t b) { char *p = sp; sp += r16(b); return p; };
     u64 *K = (u64 *)take(8 * m), *K1 = (u64 *)take(8 * m), *K2 = (u64 *)take(8 * m), *SV = (u64 *)take(8 * m);
@@ -1671,14 +1779,23 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
     const int gm = grid_for(m, 256);
     k_mm_emit_flat<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB,
                                                                n, t->thr_single, t->thr_double, counts, eoff, K, M,
-                                                               V, SV);
+                                                               V, SV, compact ? K1 : nullptr, rankA, rankB, NA, NB,
+                                                               rbits);
     k_iota<<<gm, 256, 0, st>>>(io, m);
     size_t tb1 = ctb;
-    cub::DeviceRadixSort::SortPairs(ct, tb1, K, K1, io, P1, (int)m, 0, 64, st);
-    k_gather32<<<gm, 256, 0, st>>>(M, P1, m, M1);
-    tb1 = ctb;
-    cub::DeviceRadixSort::SortPairs(ct, tb1, M1, M2, P1, P2, (int)m, 0, 32, st);
-    k_gather64<<<gm, 256, 0, st>>>(K, P2, m, K2);
+    if (compact) {
+        // one stable sort on (meta rank, colex rank): runs grouped by (meta, key), a
+        // run's records in emission (entry) order -- the same order as the two sorts
+        cub::DeviceRadixSort::SortPairs(ct, tb1, K1, K2, io, P2, (int)m, 0, kbits_all, st);
+        k_gather32<<<gm, 256, 0, st>>>(M, P2, m, M2);
+        k_gather64<<<gm, 256, 0, st>>>(K, P2, m, K2);
+    } else {
+        cub::DeviceRadixSort::SortPairs(ct, tb1, K, K1, io, P1, (int)m, 0, 64, st);
+        k_gather32<<<gm, 256, 0, st>>>(M, P1, m, M1);
+        tb1 = ctb;
+        cub::DeviceRadixSort::SortPairs(ct, tb1, M1, M2, P1, P2, (int)m, 0, 32, st);
+        k_gather64<<<gm, 256, 0, st>>>(K, P2, m, K2);
+    }
     k_mm_heads<<<gm, 256, 0, st>>>(K2, M2, m, io);        // io reused as head flags
     tb1 = ctb;
     cub::DeviceScan::InclusiveSum(ct, tb1, io, P1, (int)m, st);   // P1 reused as run ids (1-based)
@@ -1712,12 +1829,14 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
                                                          t->mm_bloom, t->mm_bloom_mask);
     cudaFreeAsync(sc, st);
     cudaFreeAsync(eoff, st);
+    cudaFreeAsync(rk, st);
     return cuda_check(cudaGetLastError(), "multimap kernels");
 }
 }  // namespace
 
 int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
     if (!h->spin.ok || t->mode != 0 || t->n == 0) return NNQS_OK;
+    t->spin_n = h->spin.n;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = t->n;
     if (n >= (1LL << 31) - 2) return NNQS_OK;
