@@ -433,3 +433,38 @@ def test_grad_weights_matches_oracle(nnqs, dev):
     tol = 1e-12 * 2 * st.counts * np.abs(_c(el)).max() / W + 1e-300
     assert np.all(np.abs(ab[:, 0] - a) <= tol) and np.all(np.abs(ab[:, 1] - b) <= tol)
     assert abs(ab[:, 0].sum()) <= 1e-9 * np.abs(ab[:, 0]).sum()
+
+
+@pytest.mark.parametrize("mixed", [False, True])
+def test_structured_heavy_paths_small(nnqs, dev, mixed, monkeypatch):
+    """The heavy-group machinery (deletion multimap with its Bloom filter, the
+    compact-key or two-sort build, the entry-driven join) forced onto C4 by low
+    thresholds (NNQS_THR_* are read at table build); with mixed=True the table
+    holds two particle sectors, so the multimap build takes the two-sort path.
+    E_loc of every row against the oracle."""
+    monkeypatch.setenv("NNQS_THR_SINGLE", "3")
+    monkeypatch.setenv("NNQS_THR_DOUBLE", "6")
+    monkeypatch.setenv("NNQS_THR_ROWHEAVY", "40")
+    m = C.molecule(4)
+    keys = S.sector_keys(10, 7, 7)
+    if mixed:
+        keys = np.concatenate([keys, S.sector_keys(10, 6, 7)])
+        order = np.lexsort((keys[:, 0], keys[:, 1]))
+        keys = np.ascontiguousarray(keys[order])
+    rng = np.random.default_rng(31)
+    lp = np.stack([rng.normal(0, 1, len(keys)), rng.uniform(-np.pi, np.pi, len(keys))], axis=1)
+    ham = ham_for(nnqs, 4)
+    tab = nnqs.nnqs_table_prepare(ham, 0, _t(keys, dev), _t(lp, dev))
+    n = len(keys)
+    stats = torch.zeros(4, dtype=torch.int64, device=dev)
+    got = _c(nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, stats_out=stats))
+    sel = np.unique(np.concatenate([np.arange(0, n, max(1, n // 600)), [n - 1]]))
+    ref, scale = R.eloc(m.h1, m.h2, m.e_core, keys[sel], lp[sel], keys=keys, logpsi=lp, with_scale=True)
+    _assert_close(got[sel], ref, scale, f"heavy paths mixed={mixed}")
+    s2 = torch.zeros(4, dtype=torch.int64, device=dev)
+    nnqs.nnqs_set_algorithm(nnqs.ALGO_LITERAL)
+    try:
+        nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, stats_out=s2)
+    finally:
+        nnqs.nnqs_set_algorithm(nnqs.ALGO_AUTO)
+    assert stats.cpu().numpy()[2] == s2.cpu().numpy()[2]     # identical hit sets
