@@ -2018,13 +2018,36 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
     u64 *hkeys = nullptr;
     void *htmp = nullptr;
     unsigned long long *hcnt = nullptr;
-    if (t->n_heavy > 0 && (phase_mask & 8)) {
-        const int64_t row_end = row_begin + n_rows;
+    const bool do_hj = t->n_heavy > 0 && (phase_mask & 8);
+    const int64_t row_end = row_begin + n_rows;
+    if (do_hj) {
         rc = cuda_check(cudaMallocAsync((void **)&acc_heavy, 16 * n_rows + 16, st), "alloc acc_heavy");
         if (!rc) rc = cuda_check(cudaMallocAsync((void **)&hcnt, 16, st), "alloc hj counter");
         if (rc) return rc;
         cudaMemsetAsync(acc_heavy, 0, 16 * n_rows, st);
         cudaMemsetAsync(hcnt, 0, 16, st);
+    }
+    // The entry-driven join (phase (iii) of the rows of very heavy alpha groups) runs on
+    // a second stream, concurrently with the phase (i)/(ii) kernels; the phase (iii)
+    // kernel waits for it.  hs waits for everything queued on st so far.
+    static cudaStream_t hs_of[64] = {};
+    cudaStream_t hs = st;
+    cudaEvent_t ev_start = nullptr, ev_hj = nullptr;
+    static int conc = -1;
+    if (conc < 0) {
+        const char *e = std::getenv("NNQS_HJ_CONCURRENT");
+        conc = e ? std::atoi(e) : 1;
+    }
+    if (do_hj && conc && h->device >= 0 && h->device < 64) {
+        if (!hs_of[h->device]) cudaStreamCreateWithFlags(&hs_of[h->device], cudaStreamNonBlocking);
+        hs = hs_of[h->device];
+        cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev_hj, cudaEventDisableTiming);
+        cudaEventRecord(ev_start, st);
+        cudaStreamWaitEvent(hs, ev_start, 0);
+    }
+    auto run_hj = [&]() -> int {
+        int rch = NNQS_OK;
         int ibits = 1, rbits = 1;
         while ((1LL << ibits) < t->n) ++ibits;
         while ((1LL << rbits) < n_rows) ++rbits;
@@ -2039,21 +2062,21 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
         }
         const dim3 hgrid(hj_gx, t->n_heavy);
         int64_t cap = std::max<int64_t>(1 << 20, std::min<int64_t>((int64_t)1 << 26, 64 * n_rows));
-        for (int attempt = 0; attempt < 2 && !rc; ++attempt) {
+        for (int attempt = 0; attempt < 2 && !rch; ++attempt) {
             size_t tb = 0;
             cub::DeviceRadixSort::SortKeys(nullptr, tb, (const u64 *)nullptr, (u64 *)nullptr, (int)cap, kbits,
-                                           kbits + ibits + rbits, st);
-            rc = cuda_check(cudaMallocAsync((void **)&hkeys, 16 * cap + tb + 8 * n_rows + 1024, st), "alloc hj keys");
-            if (rc) break;
-            cudaMemsetAsync(hcnt, 0, 8, st);
-            k_hj_emit<<<hgrid, 256, 0, st>>>(sv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end, ibits, kbits, hcnt,
+                                           kbits + ibits + rbits, hs);
+            rch = cuda_check(cudaMallocAsync((void **)&hkeys, 16 * cap + tb + 8 * n_rows + 1024, hs), "alloc hj keys");
+            if (rch) break;
+            cudaMemsetAsync(hcnt, 0, 8, hs);
+            k_hj_emit<<<hgrid, 256, 0, hs>>>(sv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end, ibits, kbits, hcnt,
                                              hkeys, cap, attempt == 0 ? (unsigned long long *)stats : nullptr);
             unsigned long long m = 0;
-            rc = cuda_check(cudaMemcpyAsync(&m, hcnt, 8, cudaMemcpyDeviceToHost, st), "read hj count");
-            if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
-            if (rc) break;
+            rch = cuda_check(cudaMemcpyAsync(&m, hcnt, 8, cudaMemcpyDeviceToHost, hs), "read hj count");
+            if (!rch) rch = cuda_check(cudaStreamSynchronize(hs), "sync");
+            if (rch) break;
             if ((int64_t)m > cap) {              // buffer too small: size exactly and redo
-                cudaFreeAsync(hkeys, st);
+                cudaFreeAsync(hkeys, hs);
                 hkeys = nullptr;
                 cap = (int64_t)m;
                 continue;
@@ -2062,24 +2085,22 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
                 u64 *k2 = hkeys + cap;
                 int32_t *kb = (int32_t *)(hkeys + 2 * cap), *ke = kb + n_rows;
                 htmp = (void *)(((uintptr_t)(ke + n_rows) + 511) & ~(uintptr_t)255);   // 256-B aligned
-                cudaMemsetAsync(kb, 0, 8 * n_rows, st);
+                cudaMemsetAsync(kb, 0, 8 * n_rows, hs);
                 tb = 0;
                 // order by (row, x' index) only: the group id rides along in the low bits
                 cub::DeviceRadixSort::SortKeys(nullptr, tb, (const u64 *)nullptr, (u64 *)nullptr, (int)m, kbits,
-                                               kbits + ibits + rbits, st);
-                cub::DeviceRadixSort::SortKeys(htmp, tb, hkeys, k2, (int)m, kbits, kbits + ibits + rbits, st);
-                k_hj_bounds<<<grid_for((int64_t)m, 256), 256, 0, st>>>(k2, (int64_t)m, ibits + kbits, kb, ke);
-                k_hj_eval<<<148 * hj_ev, 256, 0, st>>>(sv, gv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end, k2,
+                                               kbits + ibits + rbits, hs);
+                cub::DeviceRadixSort::SortKeys(htmp, tb, hkeys, k2, (int)m, kbits, kbits + ibits + rbits, hs);
+                k_hj_bounds<<<grid_for((int64_t)m, 256), 256, 0, hs>>>(k2, (int64_t)m, ibits + kbits, kb, ke);
+                k_hj_eval<<<148 * hj_ev, 256, 0, hs>>>(sv, gv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end, k2,
                                                    ibits, kbits, kb, ke, acc_heavy, (unsigned long long *)stats);
             }
             break;
         }
-        if (rc) {
-            cudaFreeAsync(acc_heavy, st);
-            cudaFreeAsync(hcnt, st);
-            return rc;
-        }
-    }
+        if (hkeys) cudaFreeAsync(hkeys, hs);
+        hkeys = nullptr;
+        return rch;
+    };
     double2 *partial = nullptr;
     rc = cuda_check(cudaMallocAsync((void **)&partial, 16 * n_rows + 16, st), "alloc partial");
     if (!rc) {
@@ -2156,18 +2177,29 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
             launch(k_eloc_spin<3, 4, true>, perm3);
             launch(k_eloc_spin<20, 4, true>, perm20);
         }
-        switch (minb % 10) {
-            case 3: launch(k_eloc_spin<24, 3, false>, perm24); break;
-            default: launch(k_eloc_spin<24, 4, false>, perm24);
+        if (do_hj) {
+            rc = run_hj();
+            if (ev_hj) {
+                cudaEventRecord(ev_hj, hs);
+                cudaStreamWaitEvent(st, ev_hj, 0);
+            }
         }
-        if (t->n_direct) launch(k_eloc_spin<24, 4, true>, perm24);
+        if (!rc) {
+            switch (minb % 10) {
+                case 3: launch(k_eloc_spin<24, 3, false>, perm24); break;
+                default: launch(k_eloc_spin<24, 4, false>, perm24);
+            }
+            if (t->n_direct) launch(k_eloc_spin<24, 4, true>, perm24);
+        }
         if (pbuf) cudaFreeAsync(pbuf, st);
         if (ctr) cudaFreeAsync(ctr, st);
         cudaFreeAsync(partial, st);
     }
+    if (ev_start) cudaEventDestroy(ev_start);
+    if (ev_hj) cudaEventDestroy(ev_hj);
     if (acc_heavy) cudaFreeAsync(acc_heavy, st);
     if (hcnt) cudaFreeAsync(hcnt, st);
-    if (hkeys) cudaFreeAsync(hkeys, st);
+    if (rc) return rc;
     return cuda_check(cudaGetLastError(), "structured local energy launch");
 }
 
