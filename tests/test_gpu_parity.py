@@ -468,3 +468,9 @@ def test_structured_heavy_paths_small(nnqs, dev, mixed, monkeypatch):
     finally:
         nnqs.nnqs_set_algorithm(nnqs.ALGO_AUTO)
     assert stats.cpu().numpy()[2] == s2.cpu().numpy()[2]     # identical hit sets
+    # degenerate slices through the same machinery: empty, one row, the last row
+    assert nnqs.nnqs_local_energy(ham, tab, 7, n_rows=0).shape[0] == 0
+    full = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n).cpu().numpy()
+    for r0 in (7, n - 1):
+        one = nnqs.nnqs_local_energy(ham, tab, r0, n_rows=1).cpu().numpy()
+        assert one.tobytes() == full[r0:r0 + 1].tobytes()
