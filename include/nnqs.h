@@ -150,7 +150,15 @@ int nnqs_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_
  *       nnqs_ham_compress: the alpha/beta-factorised enumeration (DESIGN.md
  *       "structured path"): the same (row, group) pairs with x' in the table
  *       as the literal loop, found by scanning the table's alpha-/beta-string
- *       lists; stats_out[1] then counts list entries / probes examined.
+ *       lists and probing a deletion-key multimap for heavy strings; H_xx' is
+ *       the group's Pauli sum on the in-sector folded table (R21;
+ *       diagonal and single-excitation groups in occupation form, R22), so
+ *       E_loc agrees with the literal loop to rounding (R14), not bit for bit.
+ *       stats_out[1] then counts list entries / probes examined and
+ *       stats_out[3] the folded terms evaluated.  E_loc of a row is
+ *       bit-identical for any row_begin / n_rows slicing and across runs.
+ *       The call synchronises its stream once (size of the entry-driven join)
+ *       and uses a second, library-owned stream for that join.
  *       Every other call uses the literal loop.
  *   1 -- always the literal loop of Algorithm 2 (every row x every group,
  *       sector test, hash lookup of x').
