@@ -139,6 +139,7 @@ def profile_traffic():
         return None
     tot, kernels = 0.0, []
     alu_w, t_w = 0.0, 0.0
+    per = {}
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     for block in open(TRAFFIC_FILE).read().split("## ")[1:]:
         name = block.splitlines()[0].strip()
@@ -153,9 +154,10 @@ def profile_traffic():
         if mt and ma:
             alu_w += float(mt.group(1)) * float(ma.group(1))
             t_w += float(mt.group(1))
+            per[name.replace("void ", "").replace("<unnamed>::", "")] = round(float(ma.group(1)), 1)
         kernels.append(name)
     return {"bytes_per_launch": tot, "kernels": kernels, "source": os.path.relpath(TRAFFIC_FILE, ROOT),
-            "ncu_alu_pipe_pct_time_weighted": (alu_w / t_w) if t_w else None}
+            "ncu_alu_pipe_pct_time_weighted": (alu_w / t_w) if t_w else None, "ncu_alu_pipe_pct": per}
 
 
 def cpu_baseline(mol, st, n_rows_req, seconds_target=15.0):
@@ -417,6 +419,13 @@ def run_ours(args):
                      "peak_source": f"derived: 148 SMs x 64 INT32 lanes/clk (alu pipe) x {sm_mhz:.0f} MHz "
                                     f"({src} sm_max_mhz)",
                      "algorithmic_ops_per_launch": ops_launch,
+                     "issue_utilisation": None if not per_launch_traffic else {
+                         "what": "ncu sm__inst_executed_pipe_alu % of peak (SURVEY.md 8(d)(i)), per kernel and "
+                                 "time-weighted over the local-energy call; frac above is the algorithmic "
+                                 "fraction (8(d)(ii)) reported beside it",
+                         "alu_pipe_pct_time_weighted": per_launch_traffic["ncu_alu_pipe_pct_time_weighted"],
+                         "alu_pipe_pct": per_launch_traffic["ncu_alu_pipe_pct"],
+                         "source": per_launch_traffic["source"]},
                      "ops_definition": "4 x candidates examined + 6 x (folded) Pauli strings evaluated "
                                        "(kernel counters); the kernel is bound by dependent random-access "
                                        "latency, not by a pipe (DESIGN.md Sec. 7)"},
