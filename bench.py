@@ -121,10 +121,21 @@ def peaks():
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+INT_PEAKS_FILE = os.path.join(ROOT, "profiles", "r01_int_peaks.json")
+
+
 def alu_peak_ops(sm_mhz):
-    """INT32 logic/add issue peak: 148 SMs x 4 SMSPs x 16 lanes/clk on the alu
-    pipe (LOP3/IADD3, rt_SMSP = 2; B300_MICROARCH.md 'Pipe rates') x SM clock."""
-    return 148 * 64 * sm_mhz * 1e6
+    """INT32 ALU-pipe issue peak.  Measured (scripts/microbench/int_peaks.cu on this
+    pool's B200: LOP3 throughput, 8 independent chains per thread) when the
+    committed result exists, else derived: 148 SMs x 64 lanes/clk (alu pipe,
+    B300_MICROARCH.md 'Pipe rates') x SM clock.  Returns (ops/s, source)."""
+    try:
+        d = json.load(open(INT_PEAKS_FILE))
+        return float(d["lop3_tops"]) * 1e12, (f"measured: LOP3 issue rate {d['lop3_tops']:.2f} Tops/s "
+                                              f"({os.path.relpath(INT_PEAKS_FILE, ROOT)}; POPC "
+                                              f"{d['popc_tops']:.2f}, IADD {d['iadd_tops']:.2f} Tops/s)")
+    except Exception:
+        return 148 * 64 * sm_mhz * 1e6, (f"derived: 148 SMs x 64 INT32 lanes/clk (alu pipe) x {sm_mhz:.0f} MHz")
 
 
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_local_energy_full.txt")
@@ -384,7 +395,7 @@ def run_ours(args):
     pk, src = peaks()
     clk_sum = clk.summary()
     sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
-    alu_peak = alu_peak_ops(sm_mhz)
+    alu_peak, alu_src = alu_peak_ops(sm_mhz)
     # Algorithmic integer work of one local-energy launch (rank 0's slice), from
     # the kernel's own counters: every examined candidate
     # (list entry, multimap probe, alpha-single test) needs >= 4 32-bit ops
@@ -416,8 +427,7 @@ def run_ours(args):
                      "unit": "Tops/s (INT32 ALU-pipe)", "frac": achieved / alu_peak, "traffic": per_launch_traffic,
                      "kernel": "nnqs_local_energy, structured path: k_hj_emit + CUB sort + k_hj_eval + "
                                "k_eloc_spin x4 (one launch sequence, timed with CUDA events on its stream)",
-                     "peak_source": f"derived: 148 SMs x 64 INT32 lanes/clk (alu pipe) x {sm_mhz:.0f} MHz "
-                                    f"({src} sm_max_mhz)",
+                     "peak_source": alu_src,
                      "algorithmic_ops_per_launch": ops_launch,
                      "issue_utilisation": None if not per_launch_traffic else {
                          "what": "ncu sm__inst_executed_pipe_alu % of peak (SURVEY.md 8(d)(i)), per kernel and "
