@@ -140,6 +140,7 @@ struct nnqs_table_s {
     void *mm_ent = nullptr;                    // [m] {u64 varying string, u64 entry index}, sorted by (meta, key, entry)
     void *mm_buf = nullptr;
     int32_t thr_single = 0, thr_double = 0;    // list-length thresholds
+    bool uniform_pc = false;                   // one popcount per spin over the table (set by the multimap build)
     int32_t thr_rowheavy = 0;                  // alpha groups with more rows: entry-driven phase (iii)
     int32_t *heavy_groups = nullptr;           // [n_heavy] those alpha group ids (device)
     int64_t n_alpha_groups = 0;

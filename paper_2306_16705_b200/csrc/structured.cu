@@ -122,6 +122,8 @@ struct TabSpin {
     const int2 *nl_rng;        // [alpha groups] -> [begin, end) in nl
     const int4 *nl;            // {g', u rank, offA[g'], |list(g')|} of the present a' = a ^ u
     int32_t thr_single, thr_double;
+    int uniform_pc;           // every alpha (beta) string of the table has one popcount: XOR
+                              // distance 2 / 4 already implies a balanced excitation
 };
 
 // ---------------------------------------------------------------- multimap
@@ -634,7 +636,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         const int c = __popcll(d);
                         kk[u] = -1;
                         ix[u] = 0;
-                        if ((c == 2 || c == 4) && 2 * __popcll(mine & d) == c) {
+                        if ((c == 2 || c == 4) && (T.uniform_pc || 2 * __popcll(mine & d) == c)) {
                             kk[u] = same_spin_tag(S, ph, d, c);
                             ix[u] = __ldg(lidx + j);
                         }
@@ -810,7 +812,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         const u64 d = b ^ v[u];             // before any push (candidates passing the test)
                         kk[u] = -1;
                         ix[u] = 0;
-                        if (__popcll(d) == 2 && __popcll(b & d) == 1) {
+                        if (__popcll(d) == 2 && (T.uniform_pc || __popcll(b & d) == 1)) {
                             const int r1 = __ffsll((long long)d) - 1;
                             const int r2 = 63 - __clzll((long long)d);
                             kk[u] = __ldg(S.ab_k + (int64_t)ur[u] * S.P + pair_rank(r1, r2, S.n));
@@ -1735,6 +1737,7 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
         kbits_all = rbits + mbits;
     }
     const bool compact = kbits_all <= 64 && ensure_binom(t->device) == NNQS_OK;
+    t->uniform_pc = !rc && hpc[0] == hpc[1] && hpc[2] == hpc[3];
     if (rc || m == 0) {
         cudaFreeAsync(rk, st);
         cudaFreeAsync(eoff, st);
@@ -2000,7 +2003,7 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
                t->listA_b, t->listB_a, t->listA_idx, t->listB_idx, t->ah_keys, t->ah_vals, t->ah_mask,
                (const ulonglong2 *)t->mm, t->mm_mask, t->mm_bloom, t->mm_bloom_mask,
                (const ulonglong2 *)t->mm_ent, (const int2 *)t->nl_rng, (const int4 *)t->nl, t->thr_single,
-               t->thr_double};
+               t->thr_double, t->uniform_pc ? 1 : 0};
     const int64_t threads = n_rows * 32;
     int g = (int)std::min<int64_t>((threads + 255) / 256, 148 * 64);
     if (g < 1) g = 1;
