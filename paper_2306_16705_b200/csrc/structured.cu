@@ -207,22 +207,22 @@ __device__ __forceinline__ int nth_set(u64 w, int o) {
 }
 
 // group id of the same-spin excitation d (2 or 4 bits, within one spin string)
-__device__ __forceinline__ int32_t same_spin_group(const SpinView &S, int spin, u64 d, int c) {
+// lut: shared C(p,2), C(p,3), C(p,4) for p < 64 (colex rank of a quad without
+// divisions); the extreme bits by ffs / clz, the middle two from what remains
+__device__ __forceinline__ int32_t same_spin_group(const SpinView &S, int spin, u64 d, int c, const uint32_t *lut) {
     const int p1 = __ffsll((long long)d) - 1;
-    d &= d - 1;
-    const int p2 = __ffsll((long long)d) - 1;
-    if (c == 2) return __ldg((spin ? S.pair_k1 : S.pair_k0) + pair_rank(p1, p2, S.n));
-    d &= d - 1;
-    const int p3 = __ffsll((long long)d) - 1;
-    d &= d - 1;
-    const int p4 = __ffsll((long long)d) - 1;
-    return __ldg((spin ? S.quad_k1 : S.quad_k0) + quad_rank(p1, p2, p3, p4));
+    const int p4 = 63 - __clzll((long long)d);
+    if (c == 2) return __ldg((spin ? S.pair_k1 : S.pair_k0) + pair_rank(p1, p4, S.n));
+    const u64 m = d & (d - 1) & ~(1ULL << p4);
+    const int p2 = __ffsll((long long)m) - 1;
+    const int p3 = 63 - __clzll((long long)m);
+    return __ldg((spin ? S.quad_k1 : S.quad_k0) + (p1 + (int)(lut[p2] + lut[64 + p3] + lut[128 + p4])));
 }
 
 // Queue tag of a same-spin excitation: singles with an occupation-form record
 // are queued as 0x80000000 | (spin * P + pair rank), everything else as k.
 #define OCC_TAG 0x80000000u
-__device__ __forceinline__ int32_t same_spin_tag(const SpinView &S, int spin, u64 d, int c) {
+__device__ __forceinline__ int32_t same_spin_tag(const SpinView &S, int spin, u64 d, int c, const uint32_t *lut) {
     if (c == 2 && S.occ_rec) {
         const int p1 = __ffsll((long long)d) - 1;
         const int p2 = 63 - __clzll((long long)d);
@@ -230,7 +230,7 @@ __device__ __forceinline__ int32_t same_spin_tag(const SpinView &S, int spin, u6
         if (__ldg((spin ? S.pair_k1 : S.pair_k0) + rk) < 0) return -1;
         return (int32_t)(OCC_TAG | (uint32_t)(spin * S.P + rk));
     }
-    return same_spin_group(S, spin, d, c);
+    return same_spin_group(S, spin, d, c, lut);
 }
 
 // multimap lookup: [beg, end) into mm_ent of the entries stored under (key, meta).
@@ -441,6 +441,16 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
     __shared__ int2 s_h[(PH & 8) ? WARPS_PER_BLOCK : 1][HCAP];   // heavy adjacent alpha groups (g, u rank)
     __shared__ int32_t s_pl[(PH & 8) ? WARPS_PER_BLOCK : 1][64];    // Bloom-passing probe tasks
     __shared__ RowState s_row[WARPS_PER_BLOCK];
+    __shared__ uint32_t s_lut[(PH & 6) ? 192 : 1];   // C(p,2), C(p,3), C(p,4), p < 64
+    if (PH & 6) {
+        for (int i = threadIdx.x; i < 192; i += blockDim.x) {
+            const uint32_t p = i & 63, k = 2 + (i >> 6);
+            uint32_t v = 1;
+            for (uint32_t j = 1; j <= k; ++j) v = v * (p >= k ? p - k + j : 0) / j;
+            s_lut[i] = p >= k ? v : 0;
+        }
+        __syncthreads();
+    }
     __shared__ uint8_t s_oq[(PH & 1) ? WARPS_PER_BLOCK : 1][128];   // occupied qubits (diagonal)
     __shared__ double2 s_acc[WARPS_PER_BLOCK][32];
     if ((PH & 8) && !DIRECT && stats && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(stats, pairs);
@@ -637,7 +647,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         kk[u] = -1;
                         ix[u] = 0;
                         if ((c == 2 || c == 4) && (T.uniform_pc || 2 * __popcll(mine & d) == c)) {
-                            kk[u] = same_spin_tag(S, ph, d, c);
+                            kk[u] = same_spin_tag(S, ph, d, c, s_lut);
                             ix[u] = __ldg(lidx + j);
                         }
                         c_cand += j < je;
@@ -677,7 +687,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         const ulonglong2 en = __ldg(T.mm_ent + mj);
                         idx = (int32_t)en.y;
                         const u64 d = mine ^ en.x;
-                        if (__popcll(d) == swant) k = same_spin_tag(S, ph, d, swant);
+                        if (__popcll(d) == swant) k = same_spin_tag(S, ph, d, swant, s_lut);
                     });
                 }
                 PROF_ADD(8, t_ssh)
