@@ -356,8 +356,11 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
         const u64 B0 = (u64)__double_as_longlong(__ldg(rr)), B1 = (u64)__double_as_longlong(__ldg(rr + 1));
         const double Tg = __ldg(rr + 2);
         double sum = 0.0;
-        for (u64 w = x0; w; w &= w - 1) sum += __ldg(rr + 4 + (__ffsll((long long)w) - 1));
-        for (u64 w = x1; w; w &= w - 1) sum += __ldg(rr + 68 + (__ffsll((long long)w) - 1));
+        for (int hw = 0; hw < 4; ++hw) {           // 32-bit halves: one FLO per occupied qubit
+            uint32_t w = (uint32_t)((hw < 2 ? x0 : x1) >> (32 * (hw & 1)));
+            const double *rb = rr + 4 + 32 * hw;
+            for (; w; w &= w - 1) sum += __ldg(rb + (__ffs(w) - 1));
+        }
         const double hv = flip_sign2(fma(-2.0, sum, Tg), (__popcll(x0 & B0) + __popcll(x1 & B1)) & 1);
         c_str += __popcll(x0) + __popcll(x1) + 1;
         add(hv, e.y);
