@@ -1398,6 +1398,73 @@ __global__ void __launch_bounds__(32 * NL_WARPS) k_nl(TabSpin T, int n_orb, int6
     }
 }
 
+// ---- adjacent-alpha lists by a deletion join: two alpha strings of the table are
+// one single excitation apart iff they share a 1-deletion, and they share exactly
+// one.  Each group emits its n_alpha deletions; after a sort on the deletion, every
+// run lists strings that are pairwise adjacent.
+__global__ void k_adel_count(const u64 *sa, const int32_t *listA_idx, const int32_t *offA, int64_t ng,
+                             int32_t *cnt) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x)
+        cnt[g] = __popcll(sa[listA_idx[offA[g]]]);
+}
+
+__global__ void k_adel_emit(const u64 *sa, const int32_t *listA_idx, const int32_t *offA, int64_t ng,
+                            const int32_t *eoff, u64 *DK, int32_t *DV) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x) {
+        const u64 a = sa[listA_idx[offA[g]]];
+        int32_t o = eoff[g];
+        for (u64 w = a; w; w &= w - 1, ++o) {
+            DK[o] = a ^ (w & (~w + 1));
+            DV[o] = (int32_t)g;
+        }
+    }
+}
+
+// run bounds of every sorted element, and its neighbour count (run size - 1)
+__global__ void k_adel_runs(const u64 *DK2, int64_t m, int32_t *rb, int32_t *re, int32_t *nn) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+        int64_t b = j, e = j + 1;
+        while (b > 0 && DK2[b - 1] == DK2[j]) --b;      // runs are short (<= n_empty + 1)
+        while (e < m && DK2[e] == DK2[j]) ++e;
+        rb[j] = (int32_t)b;
+        re[j] = (int32_t)e;
+        nn[j] = (int32_t)(e - b - 1);
+    }
+}
+
+__global__ void k_adel_gcount(const int32_t *G2, const int32_t *nn_g, int64_t m, int32_t *gcnt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        if (nn_g[i]) atomicAdd(gcnt + G2[i], nn_g[i]);
+}
+
+__global__ void k_adel_rng(const int32_t *beg, int64_t ng, int2 *rng) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x)
+        rng[g] = make_int2(beg[g], beg[g + 1]);
+}
+
+// element order i (sorted by group, then by deletion): write the run's other members
+__global__ void k_adel_fill(const u64 *sa, const int32_t *listA_idx, const int32_t *offA, int n_orb, int64_t m,
+                            const int32_t *G2, const int32_t *J2, const int32_t *within, const int32_t *gbeg,
+                            const int32_t *DV2, const int32_t *rb, const int32_t *re, int32_t thr_single, int4 *nl,
+                            int32_t *cost) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t g = G2[i], j = J2[i];
+        const u64 a = sa[listA_idx[offA[g]]];
+        int32_t pos = gbeg[g] + within[i];
+        int32_t work = 0;
+        for (int32_t jj = rb[j]; jj < re[j]; ++jj) {
+            if (jj == j) continue;
+            const int32_t g2 = DV2[jj];
+            const u64 a2 = sa[listA_idx[offA[g2]]];
+            const int p = __ffsll((long long)(a & ~a2)) - 1, q = __ffsll((long long)(a2 & ~a)) - 1;
+            const int32_t b0 = offA[g2], len = offA[g2 + 1] - b0;
+            nl[pos++] = make_int4(g2, pair_rank(min(p, q), max(p, q), n_orb), b0, len);
+            work += len > thr_single ? 64 : len;
+        }
+        if (work) atomicAdd(cost + g, work);
+    }
+}
+
 // per-row work estimates of the three row kernels (sort keys for a longest-first
 // row order): same-spin list lengths (probes above thr_d), adjacent-alpha work
 __global__ void k_row_cost(TabSpin T, int64_t row_begin, int64_t n_rows, int32_t thr_d, int32_t thr_rowheavy,
@@ -1946,13 +2013,85 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
         t->nl_cost = (int32_t *)((char *)t->nl_buf + rb + 64);
         t->nl = (char *)t->nl_buf + rb + 64 + cb;
         t->bytes += (int64_t)bytes;
-        cudaMemsetAsync(cursor, 0, 8, st);
-        TabSpin tv{};
-        tv.sa = t->sa; tv.listA_idx = t->listA_idx; tv.offA = t->offA;
-        tv.ah_keys = t->ah_keys; tv.ah_vals = t->ah_vals; tv.ah_mask = t->ah_mask;
-        const int gw = (int)std::min<int64_t>((ng + NL_WARPS - 1) / NL_WARPS, 148 * 48);
-        k_nl<<<std::max(gw, 1), 32 * NL_WARPS, 0, st>>>(tv, n_orb, ng, (int2 *)t->nl_rng, (int4 *)t->nl, cursor,
-                                                        t->thr_single, t->nl_cost);
+        static int nl_join = -1;
+        if (nl_join < 0) {
+            const char *e = std::getenv("NNQS_NL_JOIN");
+            nl_join = e ? std::atoi(e) : 1;
+        }
+        if (nl_join && n_orb < 64) {
+            // deletion join (see k_adel_*): ~n_alpha keys per group instead of
+            // n_alpha x n_empty hash lookups
+            int32_t *cnt = nullptr;
+            rc = cuda_check(cudaMallocAsync((void **)&cnt, 8 * (ng + 2), st), "alloc nl join counts");
+            if (rc) { cudaFreeAsync(scratch, st); return rc; }
+            int32_t *eoff = cnt + ng + 1;
+            cudaMemsetAsync(cnt + ng, 0, 4, st);
+            k_adel_count<<<grid_for(ng, 256), 256, 0, st>>>(t->sa, t->listA_idx, t->offA, ng, cnt);
+            size_t tb = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, eoff, (int)ng + 1, st);
+            void *tmp0 = nullptr;
+            rc = cuda_check(cudaMallocAsync(&tmp0, tb, st), "alloc nl join scan");
+            if (rc) { cudaFreeAsync(cnt, st); cudaFreeAsync(scratch, st); return rc; }
+            cub::DeviceScan::ExclusiveSum(tmp0, tb, cnt, eoff, (int)ng + 1, st);
+            cudaFreeAsync(tmp0, st);
+            int32_t m32 = 0;
+            rc = cuda_check(cudaMemcpyAsync(&m32, eoff + ng, 4, cudaMemcpyDeviceToHost, st), "read nl join size");
+            if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
+            if (rc) { cudaFreeAsync(cnt, st); cudaFreeAsync(scratch, st); return rc; }
+            const int64_t m = m32;
+            size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, t1, (const u64 *)nullptr, (u64 *)nullptr, (const int32_t *)nullptr,
+                                            (int32_t *)nullptr, (int)m, 0, n_orb, st);
+            cub::DeviceRadixSort::SortPairs(nullptr, t2, (const int32_t *)nullptr, (int32_t *)nullptr,
+                                            (const int32_t *)nullptr, (int32_t *)nullptr, (int)m, 0, 32, st);
+            cub::DeviceScan::ExclusiveSumByKey(nullptr, t3, (const int32_t *)nullptr, (const int32_t *)nullptr,
+                                               (int32_t *)nullptr, (int)m, cub::Equality(), st);
+            cub::DeviceScan::ExclusiveSum(nullptr, t4, (const int32_t *)nullptr, (int32_t *)nullptr, (int)ng + 1, st);
+            const size_t tt = std::max(std::max(t1, t2), std::max(t3, t4));
+            auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+            char *w = nullptr;
+            const size_t wb = 2 * al(8 * m) + 9 * al(4 * (m + 1)) + al(4 * (ng + 1)) + al(tt);
+            rc = cuda_check(cudaMallocAsync((void **)&w, wb, st), "alloc nl join work");
+            if (rc) { cudaFreeAsync(cnt, st); cudaFreeAsync(scratch, st); return rc; }
+            char *wp = w;
+            auto tk = [&](size_t x) { char *p0 = wp; wp += al(x); return p0; };
+            u64 *DK = (u64 *)tk(8 * m), *DK2 = (u64 *)tk(8 * m);
+            int32_t *DV = (int32_t *)tk(4 * (m + 1)), *DV2 = (int32_t *)tk(4 * (m + 1));
+            int32_t *rbv = (int32_t *)tk(4 * (m + 1)), *rev = (int32_t *)tk(4 * (m + 1)), *nn = (int32_t *)tk(4 * (m + 1));
+            int32_t *io = (int32_t *)tk(4 * (m + 1)), *G2 = (int32_t *)tk(4 * (m + 1)), *J2 = (int32_t *)tk(4 * (m + 1));
+            int32_t *within = (int32_t *)tk(4 * (m + 1));
+            int32_t *gcnt = (int32_t *)tk(4 * (ng + 1));
+            void *ctmp2 = tk(tt);
+            const int gm = grid_for(m, 256);
+            k_adel_emit<<<grid_for(ng, 256), 256, 0, st>>>(t->sa, t->listA_idx, t->offA, ng, eoff, DK, DV);
+            size_t tb1 = tt;
+            cub::DeviceRadixSort::SortPairs(ctmp2, tb1, DK, DK2, DV, DV2, (int)m, 0, n_orb, st);
+            k_adel_runs<<<gm, 256, 0, st>>>(DK2, m, rbv, rev, nn);
+            k_iota<<<gm, 256, 0, st>>>(io, m);
+            tb1 = tt;   // element order by group (stable: by deletion within a group)
+            cub::DeviceRadixSort::SortPairs(ctmp2, tb1, DV2, G2, io, J2, (int)m, 0, 32, st);
+            k_gather32<<<gm, 256, 0, st>>>((const uint32_t *)nn, J2, m, (uint32_t *)io);
+            tb1 = tt;   // io = nn in group order; within = its exclusive sum per group
+            cub::DeviceScan::ExclusiveSumByKey(ctmp2, tb1, G2, io, within, (int)m, cub::Equality(), st);
+            cudaMemsetAsync(gcnt, 0, 4 * (ng + 1), st);
+            k_adel_gcount<<<gm, 256, 0, st>>>(G2, io, m, gcnt);
+            tb1 = tt;
+            cub::DeviceScan::ExclusiveSum(ctmp2, tb1, gcnt, cnt, (int)ng + 1, st);   // cnt = group begin
+            k_adel_rng<<<grid_for(ng, 256), 256, 0, st>>>(cnt, ng, (int2 *)t->nl_rng);
+            cudaMemsetAsync(t->nl_cost, 0, 4 * ng, st);
+            k_adel_fill<<<gm, 256, 0, st>>>(t->sa, t->listA_idx, t->offA, n_orb, m, G2, J2, within, cnt, DV2, rbv, rev,
+                                            t->thr_single, (int4 *)t->nl, t->nl_cost);
+            cudaFreeAsync(w, st);
+            cudaFreeAsync(cnt, st);
+        } else {
+            cudaMemsetAsync(cursor, 0, 8, st);
+            TabSpin tv{};
+            tv.sa = t->sa; tv.listA_idx = t->listA_idx; tv.offA = t->offA;
+            tv.ah_keys = t->ah_keys; tv.ah_vals = t->ah_vals; tv.ah_mask = t->ah_mask;
+            const int gw = (int)std::min<int64_t>((ng + NL_WARPS - 1) / NL_WARPS, 148 * 48);
+            k_nl<<<std::max(gw, 1), 32 * NL_WARPS, 0, st>>>(tv, n_orb, ng, (int2 *)t->nl_rng, (int4 *)t->nl, cursor,
+                                                            t->thr_single, t->nl_cost);
+        }
     }
     // deletion multimap for heavy groups (sorted CSR + unique-key hash)
     rc = build_multimap(t, n, st, flags, ctmp, tmp);
