@@ -474,3 +474,28 @@ def test_structured_heavy_paths_small(nnqs, dev, mixed, monkeypatch):
     for r0 in (7, n - 1):
         one = nnqs.nnqs_local_energy(ham, tab, r0, n_rows=1).cpu().numpy()
         assert one.tobytes() == full[r0:r0 + 1].tobytes()
+
+
+def test_bench_two_ranks_shared_gpu():
+    """The N > 1 path of bench.py end to end (torchrun, 2 ranks: stage-2 all-gather,
+    rank row slices, stage-4 partials) on the one available GPU with gloo
+    (NNQS_BENCH_SHARED_GPU): the energy is bit-identical to the 1-rank run and the
+    hit counts sum to the 1-rank counts."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, NNQS_BENCH_SHARED_GPU="1")
+
+    def run(n):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+               "--master-addr", "127.0.0.1", "--master-port", str(29600 + n), "bench.py", "--gpus", str(n),
+               "--steps", "1", "--warmup", "3", "--no-cpu-baseline", "--config", "C4"]
+        out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        return json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+
+    one, two = run(1), run(2)
+    assert one["energy"] == two["energy"]
+    assert one["stats"]["hits"] == two["stats"]["hits"]
