@@ -53,6 +53,7 @@ struct SpinIndex {
     std::vector<int32_t> pair_k[2];   // [P]   2-site groups per spin
     std::vector<int32_t> quad_k[2];   // [Q]   4-site same-spin groups
     std::vector<int32_t> ab_k;        // [P*P] alpha pair x beta pair groups
+    std::vector<int32_t> ab_rec;      // [P*P] the same, or 0x40000000 | folded string for one-string groups
     // In-sector folded Pauli table (same groups, CSR): for a hit x' = x ^ X with
     // x and x' in one (N_alpha, N_beta) sector, (-1)^{popc(x & F)} is a known
     // constant for F = the pair masks of X (-1 each) or a same-spin quad (+1),
@@ -90,6 +91,7 @@ struct DeviceHam {
     int32_t *pair_k[2] = {nullptr, nullptr};
     int32_t *quad_k[2] = {nullptr, nullptr};
     int32_t *ab_k = nullptr;
+    int32_t *ab_rec = nullptr;
     double *diag_uv = nullptr; // diagonal group in occupation form (structured path)
     double *occ_rec = nullptr; // single-excitation groups in occupation form
     void *frng = nullptr;      // folded table (structured path): uint2 range per group,

@@ -80,6 +80,7 @@ struct SpinView {
     int n;
     int64_t P;
     const int32_t *pair_k0, *pair_k1, *quad_k0, *quad_k1, *ab_k;
+    const int32_t *ab_rec;    // alpha pair x beta pair -> REC_TAG | folded string (single-string groups) or k
     int32_t diag_k;
     int nq;                   // qubits
     const double *occ_rec;    // single-excitation records (SpinIndex::occ_rec) or nullptr
@@ -222,6 +223,7 @@ __device__ __forceinline__ int32_t same_spin_group(const SpinView &S, int spin, 
 // Queue tag of a same-spin excitation: singles with an occupation-form record
 // are queued as 0x80000000 | (spin * P + pair rank), everything else as k.
 #define OCC_TAG 0x80000000u
+#define REC_TAG 0x40000000   // queue key = folded string index of a one-string group (alpha x beta)
 __device__ __forceinline__ int32_t same_spin_tag(const SpinView &S, int spin, u64 d, int c, const uint32_t *lut) {
     if (c == 2 && S.occ_rec) {
         const int p1 = __ffsll((long long)d) - 1;
@@ -327,9 +329,14 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
         e = q[(qh + lane) & (QCAP - 1)];          // ring buffer: no shifting after a flush
         occ = OCC && e.x < 0;                      // single excitation, occupation-form record
         if (!occ) {
-            const uint2 be = g_range(G, e.x);
-            gb0 = be.x;
-            ge0 = be.y;
+            if (e.x & REC_TAG) {                   // single folded string, index carried in the tag
+                gb0 = (uint32_t)(e.x & ~REC_TAG);
+                ge0 = gb0 + 1;
+            } else {
+                const uint2 be = g_range(G, e.x);
+                gb0 = be.x;
+                ge0 = be.y;
+            }
         }
         if (!direct) ps0 = __ldg(psi_hat + e.y);   // issued with the offsets, used after the sum
         ++c_hit;
@@ -765,7 +772,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         if (d) {
                             const int r1 = __ffsll((long long)d) - 1;
                             const int r2 = 63 - __clzll((long long)d);
-                            k = __ldg(S.ab_k + (int64_t)sur * S.P + pair_rank(r1, r2, S.n));
+                            k = __ldg(S.ab_rec + (int64_t)sur * S.P + pair_rank(r1, r2, S.n));
                         }
                     });
                 }
@@ -828,7 +835,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         if (__popcll(d) == 2 && (T.uniform_pc || __popcll(b & d) == 1)) {
                             const int r1 = __ffsll((long long)d) - 1;
                             const int r2 = 63 - __clzll((long long)d);
-                            kk[u] = __ldg(S.ab_k + (int64_t)ur[u] * S.P + pair_rank(r1, r2, S.n));
+                            kk[u] = __ldg(S.ab_rec + (int64_t)ur[u] * S.P + pair_rank(r1, r2, S.n));
                             ix[u] = __ldg(T.listA_idx + jj[u]);
                         }
                         c_cand += (f0 + 32 * u + lane) < total;
@@ -1580,6 +1587,14 @@ int nnqs_spin_index_build(const HostTable &H, SpinIndex &S) {
         }
         S.foff[k + 1] = (uint32_t)S.fd.size();
     }
+    // ---- alpha x beta slots whose folded group is one string: the string's index
+    S.ab_rec.assign(S.ab_k.size(), -1);
+    for (size_t i = 0; i < S.ab_k.size(); ++i) {
+        const int32_t k = S.ab_k[i];
+        if (k < 0) continue;
+        const uint32_t b0 = S.foff[k], b1 = S.foff[k + 1];
+        S.ab_rec[i] = (b1 == b0 + 1 && b0 < 0x40000000u && k < 0x40000000) ? (int32_t)(0x40000000u | b0) : k;
+    }
     // ---- single-excitation groups in occupation form (see SpinIndex::occ_rec)
     S.occ_ok = N <= 128;
     if (S.occ_ok) {
@@ -1673,6 +1688,11 @@ int nnqs_spin_index_upload(nnqs_ham h) {
     if ((rc = cuda_check(cudaMalloc((void **)&D.ab_k, bab), "alloc ab_k"))) return rc;
     if ((rc = cuda_check(cudaMemcpy(D.ab_k, S.ab_k.data(), bab, cudaMemcpyHostToDevice), "copy ab_k"))) return rc;
     D.bytes += (int64_t)bab;
+    if (S.ab_rec.size() == S.ab_k.size()) {
+        if ((rc = cuda_check(cudaMalloc((void **)&D.ab_rec, bab), "alloc ab_rec"))) return rc;
+        if ((rc = cuda_check(cudaMemcpy(D.ab_rec, S.ab_rec.data(), bab, cudaMemcpyHostToDevice), "copy ab_rec"))) return rc;
+        D.bytes += (int64_t)bab;
+    }
     if (S.occ_ok) {
         const size_t bo2 = 8 * S.occ_rec.size();
         if ((rc = cuda_check(cudaMalloc((void **)&D.occ_rec, bo2), "alloc occ"))) return rc;
@@ -1717,6 +1737,8 @@ void nnqs_spin_index_release(nnqs_ham h) {
     }
     cudaFree(D.ab_k);
     D.ab_k = nullptr;
+    cudaFree(D.ab_rec);
+    D.ab_rec = nullptr;
     cudaFree(D.diag_uv);
     D.diag_uv = nullptr;
     cudaFree(D.occ_rec);
@@ -2147,7 +2169,8 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
                                   int64_t *stats, void *stream) {
     const SpinIndex &S = h->spin;
     const DeviceHam &D = h->dev;
-    SpinView sv{S.n, S.P, D.pair_k[0], D.pair_k[1], D.quad_k[0], D.quad_k[1], D.ab_k, S.diag_k,
+    SpinView sv{S.n, S.P, D.pair_k[0], D.pair_k[1], D.quad_k[0], D.quad_k[1], D.ab_k, D.ab_rec ? D.ab_rec : D.ab_k,
+                S.diag_k,
                 h->host.n_qubits, S.occ_ok ? D.occ_rec : nullptr, S.diag_K, S.diag_ok ? D.diag_uv : nullptr};
     GroupView gv{(const uint2 *)D.frng, (const ulonglong2 *)D.frec};   // in-sector folded strings
     TabSpin tv{t->n, (const ulonglong2 *)t->keys, (const double2 *)t->logpsi, (const double2 *)t->psi_hat,
