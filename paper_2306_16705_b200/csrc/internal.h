@@ -54,6 +54,7 @@ struct SpinIndex {
     std::vector<int32_t> quad_k[2];   // [Q]   4-site same-spin groups
     std::vector<int32_t> ab_k;        // [P*P] alpha pair x beta pair groups
     std::vector<int32_t> ab_rec;      // [P*P] the same, or 0x40000000 | folded string for one-string groups
+    std::vector<int32_t> quad_rec[2]; // [Q] quads: 0x40000000 | (count-1) << 28 | first folded string, or k
     // In-sector folded Pauli table (same groups, CSR): for a hit x' = x ^ X with
     // x and x' in one (N_alpha, N_beta) sector, (-1)^{popc(x & F)} is a known
     // constant for F = the pair masks of X (-1 each) or a same-spin quad (+1),
@@ -90,6 +91,7 @@ struct DeviceHam {
     // spin index (structured path)
     int32_t *pair_k[2] = {nullptr, nullptr};
     int32_t *quad_k[2] = {nullptr, nullptr};
+    int32_t *quad_rec[2] = {nullptr, nullptr};
     int32_t *ab_k = nullptr;
     int32_t *ab_rec = nullptr;
     double *diag_uv = nullptr; // diagonal group in occupation form (structured path)

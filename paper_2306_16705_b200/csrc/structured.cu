@@ -81,6 +81,7 @@ struct SpinView {
     int64_t P;
     const int32_t *pair_k0, *pair_k1, *quad_k0, *quad_k1, *ab_k;
     const int32_t *ab_rec;    // alpha pair x beta pair -> REC_TAG | folded string (single-string groups) or k
+    const int32_t *quad_rec0, *quad_rec1;   // same-spin quads -> REC_TAG | count | first string, or k
     int32_t diag_k;
     int nq;                   // qubits
     const double *occ_rec;    // single-excitation records (SpinIndex::occ_rec) or nullptr
@@ -217,13 +218,13 @@ __device__ __forceinline__ int32_t same_spin_group(const SpinView &S, int spin, 
     const u64 m = d & (d - 1) & ~(1ULL << p4);
     const int p2 = __ffsll((long long)m) - 1;
     const int p3 = 63 - __clzll((long long)m);
-    return __ldg((spin ? S.quad_k1 : S.quad_k0) + (p1 + (int)(lut[p2] + lut[64 + p3] + lut[128 + p4])));
+    return __ldg((spin ? S.quad_rec1 : S.quad_rec0) + (p1 + (int)(lut[p2] + lut[64 + p3] + lut[128 + p4])));
 }
 
 // Queue tag of a same-spin excitation: singles with an occupation-form record
 // are queued as 0x80000000 | (spin * P + pair rank), everything else as k.
 #define OCC_TAG 0x80000000u
-#define REC_TAG 0x40000000   // queue key = folded string index of a one-string group (alpha x beta)
+#define REC_TAG 0x40000000   // queue key = REC_TAG | (count - 1) << 28 | first folded string (1-4 strings)
 __device__ __forceinline__ int32_t same_spin_tag(const SpinView &S, int spin, u64 d, int c, const uint32_t *lut) {
     if (c == 2 && S.occ_rec) {
         const int p1 = __ffsll((long long)d) - 1;
@@ -329,9 +330,9 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
         e = q[(qh + lane) & (QCAP - 1)];          // ring buffer: no shifting after a flush
         occ = OCC && e.x < 0;                      // single excitation, occupation-form record
         if (!occ) {
-            if (e.x & REC_TAG) {                   // single folded string, index carried in the tag
-                gb0 = (uint32_t)(e.x & ~REC_TAG);
-                ge0 = gb0 + 1;
+            if (e.x & REC_TAG) {                   // 1-4 folded strings, start and count carried in the tag
+                gb0 = (uint32_t)(e.x & 0x0FFFFFFF);
+                ge0 = gb0 + 1 + ((e.x >> 28) & 3);
             } else {
                 const uint2 be = g_range(G, e.x);
                 gb0 = be.x;
@@ -1593,7 +1594,18 @@ int nnqs_spin_index_build(const HostTable &H, SpinIndex &S) {
         const int32_t k = S.ab_k[i];
         if (k < 0) continue;
         const uint32_t b0 = S.foff[k], b1 = S.foff[k + 1];
-        S.ab_rec[i] = (b1 == b0 + 1 && b0 < 0x40000000u && k < 0x40000000) ? (int32_t)(0x40000000u | b0) : k;
+        S.ab_rec[i] = (b1 == b0 + 1 && b0 < 0x10000000u && k < 0x40000000) ? (int32_t)(0x40000000u | b0) : k;
+    }
+    // ---- same-spin quads likewise (their folded groups hold up to 3 strings)
+    for (int sp = 0; sp < 2; ++sp) {
+        S.quad_rec[sp].assign(S.quad_k[sp].size(), -1);
+        for (size_t i = 0; i < S.quad_k[sp].size(); ++i) {
+            const int32_t k = S.quad_k[sp][i];
+            if (k < 0) continue;
+            const uint32_t b0 = S.foff[k], b1 = S.foff[k + 1];
+            S.quad_rec[sp][i] = (b1 > b0 && b1 - b0 <= 4 && b0 < 0x10000000u && k < 0x40000000)
+                                    ? (int32_t)(0x40000000u | ((b1 - b0 - 1) << 28) | b0) : k;
+        }
     }
     // ---- single-excitation groups in occupation form (see SpinIndex::occ_rec)
     S.occ_ok = N <= 128;
@@ -1682,6 +1694,12 @@ int nnqs_spin_index_upload(nnqs_ham h) {
         if ((rc = cuda_check(cudaMalloc((void **)&D.quad_k[s], bq), "alloc quad_k"))) return rc;
         if ((rc = cuda_check(cudaMemcpy(D.pair_k[s], S.pair_k[s].data(), bp, cudaMemcpyHostToDevice), "copy pair_k"))) return rc;
         if ((rc = cuda_check(cudaMemcpy(D.quad_k[s], S.quad_k[s].data(), bq, cudaMemcpyHostToDevice), "copy quad_k"))) return rc;
+        if (S.quad_rec[s].size() == S.quad_k[s].size()) {
+            if ((rc = cuda_check(cudaMalloc((void **)&D.quad_rec[s], bq), "alloc quad_rec"))) return rc;
+            if ((rc = cuda_check(cudaMemcpy(D.quad_rec[s], S.quad_rec[s].data(), bq, cudaMemcpyHostToDevice),
+                                 "copy quad_rec"))) return rc;
+            D.bytes += (int64_t)bq;
+        }
         D.bytes += (int64_t)(bp + bq);
     }
     size_t bab = 4 * S.ab_k.size();
@@ -1733,7 +1751,8 @@ void nnqs_spin_index_release(nnqs_ham h) {
     for (int s = 0; s < 2; ++s) {
         cudaFree(D.pair_k[s]);
         cudaFree(D.quad_k[s]);
-        D.pair_k[s] = D.quad_k[s] = nullptr;
+        cudaFree(D.quad_rec[s]);
+        D.pair_k[s] = D.quad_k[s] = D.quad_rec[s] = nullptr;
     }
     cudaFree(D.ab_k);
     D.ab_k = nullptr;
@@ -2170,6 +2189,7 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
     const SpinIndex &S = h->spin;
     const DeviceHam &D = h->dev;
     SpinView sv{S.n, S.P, D.pair_k[0], D.pair_k[1], D.quad_k[0], D.quad_k[1], D.ab_k, D.ab_rec ? D.ab_rec : D.ab_k,
+                D.quad_rec[0] ? D.quad_rec[0] : D.quad_k[0], D.quad_rec[1] ? D.quad_rec[1] : D.quad_k[1],
                 S.diag_k,
                 h->host.n_qubits, S.occ_ok ? D.occ_rec : nullptr, S.diag_K, S.diag_ok ? D.diag_uv : nullptr};
     GroupView gv{(const uint2 *)D.frng, (const ulonglong2 *)D.frec};   // in-sector folded strings
