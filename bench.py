@@ -427,7 +427,14 @@ def run_ours(args):
         "energy": {"mean_re": float(energy[0]), "mean_im": float(energy[1]), "var": float(energy[2]),
                    "W": float(energy[3])},
         "stats": {"row_group_pairs": int(st_local[0]), "in_sector_pairs": int(st_local[1]),
-                  "hits": int(st_local[2]), "strings_evaluated": int(st_local[3])},
+                  "hits": int(st_local[2]), "strings_evaluated": int(st_local[3]),
+                  "note": "structured path: in_sector_pairs = candidates examined (list entries, probes), "
+                          "strings_evaluated = folded terms (DESIGN.md R21/R22)"},
+        "rates_per_s": {  # per second of the local-energy call
+            "coupled_terms": int(st_local[0]) / max(world, 1) / (kern_avg_ms / 1e3),
+            "candidates_examined": int(st_local[1]) / max(world, 1) / (kern_avg_ms / 1e3),
+            "hits": int(st_local[2]) / max(world, 1) / (kern_avg_ms / 1e3),
+            "terms_evaluated": int(st_local[3]) / max(world, 1) / (kern_avg_ms / 1e3)},
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": alu_peak / 1e12,
                      "unit": "Tops/s (INT32 ALU-pipe)", "frac": achieved / alu_peak, "traffic": per_launch_traffic,
                      "kernel": "nnqs_local_energy, structured path: k_hj_emit + CUB sort + k_hj_eval + "
