@@ -435,16 +435,18 @@ def test_grad_weights_matches_oracle(nnqs, dev):
     assert abs(ab[:, 0].sum()) <= 1e-9 * np.abs(ab[:, 0]).sum()
 
 
-@pytest.mark.parametrize("mixed", [False, True])
-def test_structured_heavy_paths_small(nnqs, dev, mixed, monkeypatch):
+@pytest.mark.parametrize("mixed,rowheavy", [(False, 40), (False, 1000), (True, 1000)])
+def test_structured_heavy_paths_small(nnqs, dev, mixed, rowheavy, monkeypatch):
     """The heavy-group machinery (deletion multimap with its Bloom filter, the
-    compact-key or two-sort build, the entry-driven join) forced onto C4 by low
-    thresholds (NNQS_THR_* are read at table build); with mixed=True the table
-    holds two particle sectors, so the multimap build takes the two-sort path.
-    E_loc of every row against the oracle."""
+    compact-key or two-sort build, heavy-neighbour probes, the entry-driven join)
+    forced onto C4 by low thresholds (NNQS_THR_* are read at table build):
+    rowheavy=40 sends every row's phase (iii) through the join, 1000 through the
+    row kernel's probes; mixed=True holds two particle sectors (two-sort build,
+    no single-sector shortcut).  Two rows get psi(x) < e^-600 (DIRECT kernels).
+    E_loc of sampled rows against the oracle."""
     monkeypatch.setenv("NNQS_THR_SINGLE", "3")
     monkeypatch.setenv("NNQS_THR_DOUBLE", "6")
-    monkeypatch.setenv("NNQS_THR_ROWHEAVY", "40")
+    monkeypatch.setenv("NNQS_THR_ROWHEAVY", str(rowheavy))
     m = C.molecule(4)
     keys = S.sector_keys(10, 7, 7)
     if mixed:
@@ -453,12 +455,13 @@ def test_structured_heavy_paths_small(nnqs, dev, mixed, monkeypatch):
         keys = np.ascontiguousarray(keys[order])
     rng = np.random.default_rng(31)
     lp = np.stack([rng.normal(0, 1, len(keys)), rng.uniform(-np.pi, np.pi, len(keys))], axis=1)
+    lp[[3, 1000], 0] -= 620.0                                  # DIRECT rows (reading R11)
     ham = ham_for(nnqs, 4)
     tab = nnqs.nnqs_table_prepare(ham, 0, _t(keys, dev), _t(lp, dev))
     n = len(keys)
     stats = torch.zeros(4, dtype=torch.int64, device=dev)
     got = _c(nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, stats_out=stats))
-    sel = np.unique(np.concatenate([np.arange(0, n, max(1, n // 600)), [n - 1]]))
+    sel = np.unique(np.concatenate([np.arange(0, n, max(1, n // 600)), [3, 1000, n - 1]]))
     ref, scale = R.eloc(m.h1, m.h2, m.e_core, keys[sel], lp[sel], keys=keys, logpsi=lp, with_scale=True)
     _assert_close(got[sel], ref, scale, f"heavy paths mixed={mixed}")
     s2 = torch.zeros(4, dtype=torch.int64, device=dev)
