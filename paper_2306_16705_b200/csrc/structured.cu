@@ -1858,6 +1858,9 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
         kbits_all = rbits + mbits;
     }
     const bool compact = kbits_all <= 64 && ensure_binom(t->device) == NNQS_OK;
+    if (std::getenv("NNQS_VERBOSE"))
+        std::fprintf(stderr, "[nnqs] multimap: m=%lld kbits_all=%d rbits=%d NA=%d NB=%d pc=%d,%d,%d,%d\n", (long long)m,
+                     kbits_all, rbits, NA, NB, hpc[0], hpc[1], hpc[2], hpc[3]);
     t->uniform_pc = !rc && hpc[0] == hpc[1] && hpc[2] == hpc[3];
     if (rc || m == 0) {
         cudaFreeAsync(rk, st);
@@ -1934,6 +1937,7 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
     }
     u64 slots = 2;
     while ((double)slots < mm_load * (double)nruns) slots <<= 1;
+    if (std::getenv("NNQS_VERBOSE")) std::fprintf(stderr, "[nnqs] multimap: runs=%d slots=%llu\n", nruns, slots);
     u64 bwords = 1;
     while (bwords * 64 < 8 * (u64)nruns) bwords <<= 1;
     const size_t pbytes = r16(32 * slots) + r16(16 * m) + r16(8 * bwords);
@@ -2273,6 +2277,9 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
             rch = cuda_check(cudaMemcpyAsync(&m, hcnt, 8, cudaMemcpyDeviceToHost, hs), "read hj count");
             if (!rch) rch = cuda_check(cudaStreamSynchronize(hs), "sync");
             if (rch) break;
+            if (std::getenv("NNQS_VERBOSE"))
+                std::fprintf(stderr, "[nnqs] join: m=%llu bits=%d+%d+%d heavy_groups=%d\n", m, kbits, ibits, rbits,
+                             (int)t->n_heavy);
             if ((int64_t)m > cap) {              // buffer too small: size exactly and redo
                 cudaFreeAsync(hkeys, hs);
                 hkeys = nullptr;
