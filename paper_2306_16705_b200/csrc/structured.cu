@@ -1938,8 +1938,13 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
     u64 slots = 2;
     while ((double)slots < mm_load * (double)nruns) slots <<= 1;
     if (std::getenv("NNQS_VERBOSE")) std::fprintf(stderr, "[nnqs] multimap: runs=%d slots=%llu\n", nruns, slots);
+    static int bloom_bits = -1;   // Bloom bits per run (tuning: NNQS_BLOOM_BITS)
+    if (bloom_bits < 0) {
+        const char *e = std::getenv("NNQS_BLOOM_BITS");
+        bloom_bits = e ? std::max(1, std::atoi(e)) : 8;
+    }
     u64 bwords = 1;
-    while (bwords * 64 < 8 * (u64)nruns) bwords <<= 1;
+    while (bwords * 64 < (u64)bloom_bits * (u64)nruns) bwords <<= 1;
     const size_t pbytes = r16(32 * slots) + r16(16 * m) + r16(8 * bwords);
     rc = cuda_check(cudaMallocAsync(&t->mm_buf, pbytes, st), "alloc multimap");
     if (rc) { cudaFreeAsync(sc, st); cudaFreeAsync(eoff, st); return rc; }
