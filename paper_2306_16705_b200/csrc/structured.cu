@@ -1145,6 +1145,9 @@ __global__ void k_mm_slots(const u64 *K2, const uint32_t *M2, const int32_t *run
 // and summed per row in that order (k_hj_eval), so the result is deterministic.
 // Hit key of the join: (row - row_begin) << ibits | table index of x'; sorting
 // the keys on their used bits orders every row's hits by x' (deterministic sums).
+#ifndef HJ_FLIGHT
+#define HJ_FLIGHT 4   // matches per lane in flight (k_hj_emit)
+#endif
 __global__ void __launch_bounds__(256) k_hj_emit(SpinView S, TabSpin T, const int32_t *heavy_groups, int n_heavy,
                                                  int64_t row_begin, int64_t row_end, int ibits, int kbits,
                                                  unsigned long long *counter, u64 *keys_out, int64_t cap,
@@ -1188,9 +1191,8 @@ __global__ void __launch_bounds__(256) k_hj_emit(SpinView S, TabSpin T, const in
     unsigned long long probes = 0;
     for (long long t0 = (long long)blockIdx.x * blockDim.x; t0 < tot; t0 += (long long)gridDim.x * blockDim.x) {
         const long long t = t0 + threadIdx.x;
-        int32_t mb = 0, me = 0, idx2 = 0;
+        int32_t mb = 0, me = 0, idx2 = 0, abo = 0;
         u64 b2 = 0;
-        const int32_t *abk = S.ab_k;
         if (t < tot) {
             int lo = 0, hi = nc;                         // last c with s_pre[c] <= t
             while (hi - lo > 1) {
@@ -1202,35 +1204,76 @@ __global__ void __launch_bounds__(256) k_hj_emit(SpinView S, TabSpin T, const in
             const long long loc = t - s_pre[lo];
             const int32_t j = nl.z + (int32_t)(loc / nob);
             const int sb = (int)(loc % nob);
-            abk = S.ab_k + (int64_t)nl.y * S.P;
+            abo = nl.y;
             b2 = T.listA_b[j];
             idx2 = T.listA_idx[j];
             mm_find(T, b2 ^ (1ULL << nth_set(b2, sb)), meta, mb, me);
             ++probes;
         }
-        for (int32_t mj = mb; mj < me; ++mj) {
-            const ulonglong2 en = T.mm_ent[mj];
-            const int32_t e = (int32_t)en.y;
-            const u64 d = en.x ^ b2;
-            bool ok = e >= row_begin && e < row_end && d != 0;
-            int32_t kk = -1;
-            if (ok) {
-                const int r1 = __ffsll((long long)d) - 1, r2 = 63 - __clzll((long long)d);
-                kk = abk[pair_rank(r1, r2, S.n)];
-                ok = kk >= 0;
+        // the warp's matches, flattened over the lanes (run lengths differ widely):
+        // lane f of a step takes the f-th match in (lane, position) order
+        const int32_t len = me - mb;
+        int32_t incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int32_t excl = incl - len;
+        const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int32_t f0 = 0; f0 < total; f0 += 32 * HJ_FLIGHT) {
+            // HJ_FLIGHT matches per lane: records, then group ids, loaded before any use
+            ulonglong2 en[HJ_FLIGHT];
+            u64 bo[HJ_FLIGHT];
+            int32_t io[HJ_FLIGHT], ao[HJ_FLIGHT];
+#pragma unroll
+            for (int u = 0; u < HJ_FLIGHT; ++u) {
+                const int32_t f = f0 + 32 * u + lane;
+                int lo = 0;
+#pragma unroll
+                for (int st = 16; st; st >>= 1) {
+                    const int c = lo + st;
+                    const int32_t ex = __shfl_sync(0xffffffffu, excl, c & 31);
+                    if (c < 32 && ex <= f) lo = c;
+                }
+                const int32_t mj = __shfl_sync(0xffffffffu, mb, lo) + (f - __shfl_sync(0xffffffffu, excl, lo));
+                bo[u] = __shfl_sync(0xffffffffu, b2, lo);
+                io[u] = __shfl_sync(0xffffffffu, idx2, lo);
+                ao[u] = __shfl_sync(0xffffffffu, abo, lo);
+                en[u] = f < total ? T.mm_ent[mj] : make_ulonglong2(bo[u], 0);   // d = 0: no hit
             }
-            // warp-aggregated slot reservation among the lanes still in this loop
-            const unsigned act = __activemask();
-            const unsigned m = __ballot_sync(act, ok);
+            int32_t kk[HJ_FLIGHT];
+#pragma unroll
+            for (int u = 0; u < HJ_FLIGHT; ++u) {
+                const int32_t e = (int32_t)en[u].y;
+                const u64 d = en[u].x ^ bo[u];
+                kk[u] = -1;
+                if (e >= row_begin && e < row_end && d != 0) {
+                    const int r1 = __ffsll((long long)d) - 1, r2 = 63 - __clzll((long long)d);
+                    kk[u] = S.ab_k[(int64_t)ao[u] * S.P + pair_rank(r1, r2, S.n)];
+                }
+            }
+            // one warp-aggregated slot reservation for all HJ_FLIGHT x 32 matches
+            unsigned m[HJ_FLIGHT];
+            int nok = 0;
+#pragma unroll
+            for (int u = 0; u < HJ_FLIGHT; ++u) {
+                m[u] = __ballot_sync(0xffffffffu, kk[u] >= 0);
+                nok += __popc(m[u]);
+            }
             unsigned long long base = 0;
-            const int leader = __ffs(act) - 1;
-            if (lane == leader && m) base = atomicAdd(counter, (unsigned long long)__popc(m));
-            base = __shfl_sync(act, base, leader);
-            if (ok) {
-                const unsigned long long slot = base + __popc(m & ((1u << lane) - 1u));
-                if ((int64_t)slot < cap)
-                    keys_out[slot] = ((((u64)(e - row_begin) << ibits) | (u64)(uint32_t)idx2) << kbits) |
-                                     (kbits ? (u64)(uint32_t)kk : 0);
+            if (lane == 0 && nok) base = atomicAdd(counter, (unsigned long long)nok);
+            base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+            for (int u = 0; u < HJ_FLIGHT; ++u) {
+                if (kk[u] >= 0) {
+                    const unsigned long long slot = base + __popc(m[u] & ((1u << lane) - 1u));
+                    if ((int64_t)slot < cap)
+                        keys_out[slot] =
+                            ((((u64)((int32_t)en[u].y - row_begin) << ibits) | (u64)(uint32_t)io[u]) << kbits) |
+                            (kbits ? (u64)(uint32_t)kk[u] : 0);
+                }
+                base += __popc(m[u]);
             }
         }
     }
