@@ -15,6 +15,8 @@
  *                        (P:139-141), fused entry evaluation,
  *                        sample-aware: x' not in the table contributes 0
  *                        (P:379); Algorithm 2.  Device.
+ *   nnqs_chunk_work      per-chunk work estimate for cost-balanced rank
+ *                        slices (the data-centric split).  Device.
  *   nnqs_energy_reduce   count-weighted mean and variance, Eq. (6)
  *                        over unique samples with weights.  Device.
  *
@@ -175,6 +177,20 @@ int nnqs_get_algorithm(void);
  * reading.  Synchronises the device.  Returns NNQS_OK or NNQS_E_CUDA.
  */
 int nnqs_debug_counters(uint64_t *out, int reset);
+
+/*
+ * Work estimate of nnqs_local_energy per chunk of table rows, for cost-balanced
+ * contiguous rank slices (the paper's ist / batch_size_cur_rank, P:389, P:425,
+ * with slice lengths chosen by work instead of by count: rows near the
+ * Hartree-Fock string couple to far more table entries than the rest, and the
+ * sorted table puts them together).  work_out: host i64[ceil(n/chunk)], chunk c
+ * covering rows [c*chunk, min((c+1)*chunk, n)); relative units (list lengths
+ * the row kernels scan, fixed costs for probed lists and join rows; the literal
+ * Algorithm 2 path: rows per chunk).  Deterministic for a given table, so every
+ * rank derives the same slices.  Synchronises cuda_stream.  NNQS_E_ARG on bad
+ * arguments (chunk <= 0), NNQS_E_CUDA on a launch or copy failure.
+ */
+int nnqs_chunk_work(nnqs_table t, int64_t chunk, int64_t *work_out, void *cuda_stream);
 
 /* Synchronises cuda_stream; NNQS_E_ZERO_PSI if any of eloc (device f64[n][2]) is NaN. */
 int nnqs_local_energy_check(const double *eloc, int64_t n, void *cuda_stream);

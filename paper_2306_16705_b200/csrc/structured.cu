@@ -440,13 +440,16 @@ __device__ unsigned long long g_prof[16];
 // spin lists, 8 alpha x beta.  PH = 7 writes the row's partial sum to
 // `partial`; PH = 8 starts from it and finalises E_loc (two smaller kernels:
 // fewer registers, more resident warps, less instruction-cache pressure).
+// partial2 != NULL: phase (ii) (PH = 20) runs concurrently with PH = 3 on its own
+// stream, starts from zero and writes partial2; PH = 24 starts from
+// partial + partial2 (a row's order is still fixed by the row and the table).
 template <int PH, int MINB, bool DIRECT>
 __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G, TabSpin T, int64_t row_begin,
                                                    int64_t n_rows, double2 *out,
                                                    unsigned long long *stats, unsigned long long pairs,
                                                    int phase_mask, const double2 *acc_heavy, int32_t thr_rowheavy,
                                                    double2 *partial, unsigned long long *row_ctr,
-                                                   const int32_t *perm) {
+                                                   const int32_t *perm, double2 *partial2) {
     __shared__ int2 s_q[WARPS_PER_BLOCK][QCAP];
     __shared__ uint8_t s_orb[WARPS_PER_BLOCK][4][64];   // occ(a), vir(a), occ(b), vir(b) of the row
     __shared__ int2 s_h[(PH & 8) ? WARPS_PER_BLOCK : 1][HCAP];   // heavy adjacent alpha groups (g, u rank)
@@ -508,7 +511,18 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             rs->lx = lx0;
             rs->direct = DIRECT;
         }
-        acc[lane] = ((PH & 16) && lane == 0) ? partial[r] : make_double2(0.0, 0.0);   // 16: continue a row
+        double2 a0 = make_double2(0.0, 0.0);         // 16: continue a row
+        if ((PH & 16) && lane == 0) {
+            if (!(PH & 8) && partial2) {
+                // phase (ii) concurrent with (i): starts from zero
+            } else if ((PH & 8) && partial2) {
+                const double2 p1 = partial[r], p2 = partial2[r];
+                a0 = make_double2(p1.x + p2.x, p1.y + p2.y);
+            } else {
+                a0 = partial[r];
+            }
+        }
+        acc[lane] = a0;
         for (int j = lane; j < S.n; j += 32) {       // orbital lists (replace nth-set-bit searches)
             const u64 below = (1ULL << j) - 1;
             if ((a >> j) & 1) occA[__popcll(a & below)] = (uint8_t)j;
@@ -862,7 +876,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             ar += __shfl_xor_sync(0xffffffffu, ar, o);
             ai += __shfl_xor_sync(0xffffffffu, ai, o);
         }
-        if (lane == 0 && !(PH & 8)) partial[r] = make_double2(ar, ai);
+        if (lane == 0 && !(PH & 8)) (((PH & 16) && partial2) ? partial2 : partial)[r] = make_double2(ar, ai);
         if (lane == 0 && (PH & 8)) {
             double2 e;
             if (direct) {
@@ -1149,8 +1163,8 @@ __global__ void k_mm_slots(const u64 *K2, const uint32_t *M2, const int32_t *run
 #define HJ_FLIGHT 4   // matches per lane in flight (k_hj_emit)
 #endif
 __global__ void __launch_bounds__(256) k_hj_emit(SpinView S, TabSpin T, const int32_t *heavy_groups, int n_heavy,
-                                                 int64_t row_begin, int64_t row_end, int ibits, int kbits,
-                                                 unsigned long long *counter, u64 *keys_out, int64_t cap,
+                                                 int64_t row_begin, int64_t row_end, int clip, int ibits,
+                                                 int kbits, unsigned long long *counter, u64 *keys_out, int64_t cap,
                                                  unsigned long long *stats) {
     // (heavy group g = blockIdx.y): the tasks (adjacent alpha string a', entry of
     // list(a'), occupied beta orbital of the entry) of all of g's adjacent strings
@@ -1209,6 +1223,22 @@ __global__ void __launch_bounds__(256) k_hj_emit(SpinView S, TabSpin T, const in
             idx2 = T.listA_idx[j];
             mm_find(T, b2 ^ (1ULL << nth_set(b2, sb)), meta, mb, me);
             ++probes;
+            if (clip && me > mb) {
+                // a run's records are in table-entry order: keep only this rank's rows
+                // (the same matches the filter below keeps, without loading the others)
+                int32_t lo = mb, hi = me;
+                while (lo < hi) {
+                    const int32_t mid = (lo + hi) >> 1;
+                    if ((int64_t)(int32_t)T.mm_ent[mid].y < row_begin) lo = mid + 1; else hi = mid;
+                }
+                int32_t lo2 = lo, hi2 = me;
+                while (lo2 < hi2) {
+                    const int32_t mid = (lo2 + hi2) >> 1;
+                    if ((int64_t)(int32_t)T.mm_ent[mid].y < row_end) lo2 = mid + 1; else hi2 = mid;
+                }
+                mb = lo;
+                me = lo2;
+            }
         }
         // the warp's matches, flattened over the lanes (run lengths differ widely):
         // lane f of a step takes the f-th match in (lane, position) order
@@ -1530,6 +1560,27 @@ __global__ void k_row_cost(TabSpin T, int64_t row_begin, int64_t n_rows, int32_t
         c24[r] = la > thr_rowheavy ? 0u : (uint32_t)nl_cost[ga];
         iota[r] = (int32_t)r;
     }
+}
+
+// per-chunk work estimate of the three row kernels and the entry-driven join (for
+// cost-balanced rank slices): per row base + beta-side list (phase i) + alpha-side
+// list (phase ii) + adjacent-alpha work (phase iii); lists above thr_d are probed
+// (cost pd), rows of join-evaluated alpha groups cost pj.  One block per chunk.
+__global__ void __launch_bounds__(256) k_chunk_work(TabSpin T, int64_t chunk, int32_t thr_d, int32_t thr_rowheavy,
+                                                    const int32_t *nl_cost, int32_t w0, int32_t pd, int32_t pj,
+                                                    long long *work) {
+    const int64_t r0 = (int64_t)blockIdx.x * chunk;
+    const int64_t r1 = (r0 + chunk < T.n) ? r0 + chunk : T.n;
+    long long w = 0;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        const int32_t ga = T.ga_of[i], gb = T.gb_of[i];
+        const int32_t la = T.offA[ga + 1] - T.offA[ga], lb = T.offB[gb + 1] - T.offB[gb];
+        w += w0 + (lb > thr_d ? pd : lb) + (la > thr_d ? pd : la) + (la > thr_rowheavy ? pj : (nl_cost ? nl_cost[ga] : 0));
+    }
+    typedef cub::BlockReduce<long long, 256> Red;
+    __shared__ typename Red::TempStorage tmp;
+    const long long tot = Red(tmp).Sum(w);
+    if (threadIdx.x == 0) work[blockIdx.x] = tot;
 }
 
 __global__ void k_find_heavy(const int32_t *listA_idx, const int32_t *ga_of, const int32_t *offA, int64_t n,
@@ -2236,6 +2287,33 @@ void nnqs_table_release_spin(nnqs_table t) {
     t->spin_ready = false;
 }
 
+int nnqs_chunk_work_spin(nnqs_table t, int64_t chunk, int64_t *work_host, void *stream) {
+    const int64_t nch = (t->n + chunk - 1) / chunk;
+    if (nch == 0) return NNQS_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    static int w0 = -1, pd = -1, pj = -1;   // estimate weights (measurement knobs: NNQS_WORK_W0/PD/PJ)
+    if (w0 < 0) {
+        const char *a = std::getenv("NNQS_WORK_W0"), *b = std::getenv("NNQS_WORK_PD"), *c = std::getenv("NNQS_WORK_PJ");
+        w0 = a ? std::atoi(a) : 256;
+        pd = b ? std::atoi(b) : 4096;
+        pj = c ? std::atoi(c) : 4096;
+    }
+    TabSpin tv{};
+    tv.n = t->n;
+    tv.ga_of = t->ga_of;
+    tv.gb_of = t->gb_of;
+    tv.offA = t->offA;
+    tv.offB = t->offB;
+    long long *wd = nullptr;
+    int rc = cuda_check(cudaMallocAsync((void **)&wd, 8 * nch, st), "alloc chunk work");
+    if (rc) return rc;
+    k_chunk_work<<<(unsigned)nch, 256, 0, st>>>(tv, chunk, t->thr_double, t->thr_rowheavy, t->nl_cost, w0, pd, pj, wd);
+    rc = cuda_check(cudaMemcpyAsync(work_host, wd, 8 * nch, cudaMemcpyDeviceToHost, st), "read chunk work");
+    cudaFreeAsync(wd, st);
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync chunk work");
+    return rc;
+}
+
 int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, int64_t n_rows, double *eloc,
                                   int64_t *stats, void *stream) {
     const SpinIndex &S = h->spin;
@@ -2310,6 +2388,11 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
             hj_gx = e1 ? std::atoi(e1) : 1184;
             hj_ev = e2 ? std::atoi(e2) : 8;
         }
+        static int hj_clip = -1;   // clip matched runs to this rank's rows (measurement knob: NNQS_HJ_CLIP)
+        if (hj_clip < 0) {
+            const char *e = std::getenv("NNQS_HJ_CLIP");
+            hj_clip = e ? std::atoi(e) : 1;
+        }
         const dim3 hgrid(hj_gx, t->n_heavy);
         int64_t cap = std::max<int64_t>(1 << 20, std::min<int64_t>((int64_t)1 << 26, 64 * n_rows));
         for (int attempt = 0; attempt < 2 && !rch; ++attempt) {
@@ -2319,7 +2402,8 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
             rch = cuda_check(cudaMallocAsync((void **)&hkeys, 16 * cap + tb + 8 * n_rows + 1024, hs), "alloc hj keys");
             if (rch) break;
             cudaMemsetAsync(hcnt, 0, 8, hs);
-            k_hj_emit<<<hgrid, 256, 0, hs>>>(sv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end, ibits, kbits, hcnt,
+            k_hj_emit<<<hgrid, 256, 0, hs>>>(sv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end,
+                                             (int)(hj_clip && (row_begin > 0 || row_end < t->n)), ibits, kbits, hcnt,
                                              hkeys, cap, attempt == 0 ? (unsigned long long *)stats : nullptr);
             unsigned long long m = 0;
             rch = cuda_check(cudaMemcpyAsync(&m, hcnt, 8, cudaMemcpyDeviceToHost, hs), "read hj count");
@@ -2355,7 +2439,19 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
         return rch;
     };
     double2 *partial = nullptr;
-    rc = cuda_check(cudaMallocAsync((void **)&partial, 16 * n_rows + 16, st), "alloc partial");
+    static int par12 = -1;   // phases (i) and (ii) on two streams (NNQS_PAR12; 0 = one chain)
+    if (par12 < 0) {
+        const char *e = std::getenv("NNQS_PAR12");
+        par12 = e ? std::atoi(e) : 1;
+    }
+    static cudaStream_t s2_of[64] = {};
+    cudaStream_t s2 = nullptr;
+    if (par12 && h->device >= 0 && h->device < 64) {
+        if (!s2_of[h->device]) cudaStreamCreateWithFlags(&s2_of[h->device], cudaStreamNonBlocking);
+        s2 = s2_of[h->device];
+    }
+    rc = cuda_check(cudaMallocAsync((void **)&partial, (s2 ? 32 : 16) * n_rows + 32, st), "alloc partial");
+    double2 *partial2 = (s2 && !rc) ? partial + n_rows + 1 : nullptr;
     if (!rc) {
         static int minb = -1;   // resident blocks/SM of the two instantiations (tuning only)
         if (minb < 0) {
@@ -2408,27 +2504,40 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
             cudaMemsetAsync(ctr, 0, 64, st);
         }
         int nl = 0;
-        auto launch = [&](auto kern, const int32_t *perm) {
+        cudaEvent_t ev_p0 = nullptr, ev_p2 = nullptr;
+        if (s2) {   // s2 starts after everything before (row orders, counters, partial buffer)
+            cudaEventCreateWithFlags(&ev_p0, cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&ev_p2, cudaEventDisableTiming);
+            cudaEventRecord(ev_p0, st);
+            cudaStreamWaitEvent(s2, ev_p0, 0);
+        }
+        auto launch = [&](auto kern, const int32_t *perm, cudaStream_t ks) {
             int gg = g;
             if (dyn) {
                 int per_sm = 0;
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
                 gg = std::max(1, per_sm) * 148;
             }
-            kern<<<gg, 256, 0, st>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc, (unsigned long long *)stats,
+            kern<<<gg, 256, 0, ks>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc, (unsigned long long *)stats,
                                      pairs, phase_mask, acc_heavy, t->thr_rowheavy, partial, ctr ? ctr + nl : nullptr,
-                                     ctr ? perm : nullptr);
+                                     ctr ? perm : nullptr, partial2);
             ++nl;
         };
         // three launches, each a smaller kernel (instruction cache): diagonal + phase (i)
         // -> partial; phase (ii) adds; phase (iii) adds and finalises
+        // (with s2: phase (ii) on s2, concurrent with phase (i); joined before phase (iii))
+        cudaStream_t s20 = s2 ? s2 : st;
         switch (minb / 10) {
-            case 3: launch(k_eloc_spin<3, 3, false>, perm3); launch(k_eloc_spin<20, 3, false>, perm20); break;
-            default: launch(k_eloc_spin<3, 4, false>, perm3); launch(k_eloc_spin<20, 4, false>, perm20);
+            case 3: launch(k_eloc_spin<3, 3, false>, perm3, st); launch(k_eloc_spin<20, 3, false>, perm20, s20); break;
+            default: launch(k_eloc_spin<3, 4, false>, perm3, st); launch(k_eloc_spin<20, 4, false>, perm20, s20);
         }
         if (t->n_direct) {
-            launch(k_eloc_spin<3, 4, true>, perm3);
-            launch(k_eloc_spin<20, 4, true>, perm20);
+            launch(k_eloc_spin<3, 4, true>, perm3, st);
+            launch(k_eloc_spin<20, 4, true>, perm20, s20);
+        }
+        if (s2) {
+            cudaEventRecord(ev_p2, s2);
+            cudaStreamWaitEvent(st, ev_p2, 0);
         }
         if (do_hj) {
             rc = run_hj();
@@ -2439,11 +2548,13 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
         }
         if (!rc) {
             switch (minb % 10) {
-                case 3: launch(k_eloc_spin<24, 3, false>, perm24); break;
-                default: launch(k_eloc_spin<24, 4, false>, perm24);
+                case 3: launch(k_eloc_spin<24, 3, false>, perm24, st); break;
+                default: launch(k_eloc_spin<24, 4, false>, perm24, st);
             }
-            if (t->n_direct) launch(k_eloc_spin<24, 4, true>, perm24);
+            if (t->n_direct) launch(k_eloc_spin<24, 4, true>, perm24, st);
         }
+        if (ev_p0) cudaEventDestroy(ev_p0);
+        if (ev_p2) cudaEventDestroy(ev_p2);
         if (pbuf) cudaFreeAsync(pbuf, st);
         if (ctr) cudaFreeAsync(ctr, st);
         cudaFreeAsync(partial, st);

@@ -30,6 +30,35 @@ def shard_bounds(n_rows: int, world: int, rank: int, chunk: int = REDUCE_CHUNK):
     return min(lo * chunk, n_rows), min(hi * chunk, n_rows)
 
 
+def balanced_bounds(work, world: int, rank: int, chunk: int = REDUCE_CHUNK, n_rows: int | None = None):
+    """Contiguous, chunk-aligned slice [begin, end) of the table rows for this rank
+    with about equal estimated work (nnqs_chunk_work: one int64 per chunk): rank r
+    starts at the first chunk whose work prefix reaches r/world of the total.  Pure
+    integer arithmetic on the replicated estimate, so every rank derives the same
+    slices; chunk alignment keeps the energy bit-identical to 1 GPU."""
+    w = [int(v) for v in work]
+    n_chunks = len(w)
+    n = n_chunks * chunk if n_rows is None else n_rows
+    total = sum(w)
+    if total <= 0:
+        return shard_bounds(n, world, rank, chunk)
+
+    def start(r):
+        if r <= 0:
+            return 0
+        if r >= world:
+            return n_chunks
+        target = total * r   # first c with world * prefix(c) >= total * r
+        acc = 0
+        for c in range(n_chunks):
+            if acc * world >= target:
+                return c
+            acc += w[c]
+        return n_chunks
+
+    return min(start(rank) * chunk, n), min(start(rank + 1) * chunk, n)
+
+
 def all_gather_varlen(t: torch.Tensor, group=None) -> torch.Tensor:
     """all_gather_into_tensor of per-rank tensors with different first
     dimensions: gather the lengths, pad to the maximum, gather, strip."""

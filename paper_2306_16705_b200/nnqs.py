@@ -35,6 +35,7 @@ _sig = {
     "nnqs_table_info": ([P, P, P, P], ctypes.c_int),
     "nnqs_local_energy": ([P, P, I64, P, P, I64, P, P, P], ctypes.c_int),
     "nnqs_local_energy_check": ([P, I64, P], ctypes.c_int),
+    "nnqs_chunk_work": ([P, I64, P, P], ctypes.c_int),
     "nnqs_set_algorithm": ([ctypes.c_int], ctypes.c_int),
     "nnqs_get_algorithm": ([], ctypes.c_int),
     "nnqs_debug_counters": ([P, ctypes.c_int], ctypes.c_int),
@@ -226,6 +227,14 @@ def nnqs_debug_counters(reset: bool = True):
     out = np.zeros(16, dtype=np.uint64)
     _check(_lib.nnqs_debug_counters(out.ctypes.data, int(bool(reset))))
     return out
+
+
+def nnqs_chunk_work(table: Table, chunk: int = REDUCE_CHUNK, stream=None):
+    """Host int64[ceil(n/chunk)] work estimate per chunk of table rows (see include/nnqs.h)."""
+    import numpy as np
+    out = np.zeros(max((table.n + chunk - 1) // chunk, 1), dtype=np.int64)
+    _check(_lib.nnqs_chunk_work(table.handle, int(chunk), out.ctypes.data, _stream(stream)))
+    return out[: (table.n + chunk - 1) // chunk]
 
 
 def nnqs_local_energy_check(eloc, stream=None):
