@@ -57,7 +57,7 @@ def config_dict(name, mol, st, world, extra=None):
     d = {"workload": f"{name}: {mol.name}, N={mol.n_qubits} spin orbitals, N_u={len(st.keys)} unique samples, "
                      f"sample-aware mode, rows = all table entries sharded over ranks",
          "n_spin_orbitals": mol.n_qubits, "n_unique": int(len(st.keys)), "n_rows": int(len(st.keys)),
-         "n_samples": int(st.counts.sum()), "parallelism": f"dp{world} (rows sharded, table replicated)",
+         "n_samples": int(st.counts.sum()), "parallelism": f"dp{world} (rows sharded in work-balanced contiguous slices, table replicated)",
          "l2": "flushed between timed steps (256 MiB write outside the per-step events)"}
     if extra:
         d.update(extra)
@@ -289,26 +289,33 @@ def run_ours(args):
     keys_d, lp_d, cnt_d = keys_h.to(dev), lp_h.to(dev), cnt_h.to(dev)
     n_local = e - b
     stream = torch.cuda.current_stream()
-    eloc = torch.empty((n_local, 2), dtype=torch.float64, device=dev)
+    eloc = torch.empty((n if world > 1 else n_local, 2), dtype=torch.float64, device=dev)
+    rows_of = {"b": b, "e": e}   # rows this rank evaluates (world > 1: work-balanced, per step)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ev_k = []          # (start, end) events around nnqs_local_energy
 
     def step(kd, ld, cd, timed):
         if world > 1:
             gk, gl = D.gather_samples(kd, ld)
+            gc = D.gather_counts(cd)
         else:
             gk, gl = kd, ld
         tab = nnqs.nnqs_table_prepare(ham, 0, gk, gl, stream=stream)
+        rb, re_ = b, e
+        if world > 1:   # contiguous chunk-aligned slice of about equal estimated work
+            rb, re_ = D.balanced_bounds(nnqs.nnqs_chunk_work(tab, stream=stream), world, rank, n_rows=n)
+            rows_of["b"], rows_of["e"] = rb, re_
+        el = eloc[: re_ - rb]
         if timed:
             s0 = torch.cuda.Event(enable_timing=True)
             s1 = torch.cuda.Event(enable_timing=True)
             s0.record(stream)
-        nnqs.nnqs_local_energy(ham, tab, b, n_rows=n_local, eloc_out=eloc, stream=stream)
+        nnqs.nnqs_local_energy(ham, tab, rb, n_rows=re_ - rb, eloc_out=el, stream=stream)
         if timed:
             s1.record(stream)
             ev_k.append((s0, s1))
         if world > 1:
-            en = D.distributed_energy(eloc, cd, stream=stream)
+            en = D.distributed_energy(el, gc[rb:re_], stream=stream)
         else:
             part = nnqs.nnqs_energy_chunk_partials(eloc, cd, stream=stream)
             m1 = nnqs.nnqs_energy_combine(part, 1, stream=stream)
@@ -347,7 +354,8 @@ def run_ours(args):
     energy = en.cpu().numpy()
     # stats of one launch (not timed)
     tab = nnqs.nnqs_table_prepare(ham, 0, *(D.gather_samples(keys_d, lp_d) if world > 1 else (keys_d, lp_d)))
-    nnqs.nnqs_local_energy(ham, tab, b, n_rows=n_local, eloc_out=eloc, stats_out=stats)
+    nnqs.nnqs_local_energy(ham, tab, rows_of["b"], n_rows=rows_of["e"] - rows_of["b"],
+                           eloc_out=eloc[: rows_of["e"] - rows_of["b"]], stats_out=stats)
     st_local = stats.cpu().numpy().astype(np.int64)
     tab.close()
 

@@ -96,6 +96,12 @@ def gather_samples(local_keys: torch.Tensor, local_logpsi: torch.Tensor, group=N
     return unpack_records(rec)
 
 
+def gather_counts(local_counts: torch.Tensor, group=None) -> torch.Tensor:
+    """Sample multiplicities of every rank's shard, in rank order (needed when the
+    evaluated row slice, balanced_bounds, differs from the owned sample shard)."""
+    return all_gather_varlen(local_counts.reshape(-1, 1), group).reshape(-1)
+
+
 def distributed_energy(eloc_local: torch.Tensor, counts_local: torch.Tensor, group=None, stream=None):
     """Stage 4: count-weighted mean and variance (Eq. 6) over all
     ranks' rows.  Returns a device f64[4] = (mean_re, mean_im, var, W)."""

@@ -77,6 +77,52 @@ def _partials_case(rank, world):
     return allp[:, 0].tolist()
 
 
+def _balanced_case(rank, world):
+    """Every rank derives the same work-balanced slices from the replicated estimate;
+    their chunk partials, gathered in rank order, are the global chunk sequence, and
+    the gathered counts equal the global counts."""
+    n = 37 * 1024 + 5
+    rng = np.random.default_rng(7)
+    work = rng.integers(1, 1000, size=(n + 1023) // 1024)
+    work[0] = 50_000                              # one heavy chunk (the Hartree-Fock row)
+    b, e = D.balanced_bounds(work, world, rank, n_rows=n)
+    bs = D.all_gather_varlen(torch.tensor([[b, e]], dtype=torch.int64))
+    chunks = torch.arange(b // 1024, (e + 1023) // 1024, dtype=torch.float64).reshape(-1, 1).repeat(1, 3)
+    allp = D.all_gather_varlen(chunks)
+    cnt = np.arange(n, dtype=np.int64) % 5
+    sb, se = D.shard_bounds(n, world, rank)
+    gc = D.gather_counts(torch.from_numpy(cnt[sb:se]))
+    return bs.tolist(), allp[:, 0].tolist(), bool(np.array_equal(gc.numpy(), cnt))
+
+
+def test_balanced_bounds_world2():
+    out = _run(_balanced_case)
+    n_chunks = (37 * 1024 + 5 + 1023) // 1024
+    assert out[0] == out[1]
+    bs, seq, ok = out[0]
+    assert bs[0][0] == 0 and bs[-1][1] == 37 * 1024 + 5 and bs[0][1] == bs[1][0]
+    assert seq == [float(c) for c in range(n_chunks)] and ok
+
+
+def test_balanced_bounds_cover_align_balance():
+    rng = np.random.default_rng(3)
+    for n in (1, 1023, 1024, 10 * 1024 + 77, 300 * 1024):
+        nch = (n + 1023) // 1024
+        for work in (rng.integers(0, 100, size=nch), np.ones(nch, np.int64), np.zeros(nch, np.int64),
+                     np.r_[10**6, np.ones(nch - 1, np.int64)]):
+            for world in (1, 2, 3, 4, 8):
+                bs = [D.balanced_bounds(work, world, r, n_rows=n) for r in range(world)]
+                assert bs[0][0] == 0 and bs[-1][1] == n
+                for (b0, e0), (b1, e1) in zip(bs[:-1], bs[1:]):
+                    assert e0 == b1 and (b1 % 1024 == 0 or b1 == n)
+                assert all(b <= e for b, e in bs)
+                tot = int(work.sum())
+                if tot:   # no slice exceeds its share by more than one chunk's work
+                    for b, e in bs:
+                        w = int(work[b // 1024:(e + 1023) // 1024].sum())
+                        assert w * world <= tot + world * int(work.max())
+
+
 def test_shard_bounds_cover_and_align():
     for n in (0, 1, 1023, 1024, 10 * 1024 + 77, 10**6):
         for world in (1, 2, 3, 4, 8):

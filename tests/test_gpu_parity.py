@@ -209,6 +209,15 @@ def test_c5_bitwise_determinism_and_slices(nnqs, dev, c5):
                         for s0, s1 in zip(cuts[:-1], cuts[1:])])
     assert a.tobytes() == b.tobytes()
     assert a.tobytes() == d.tobytes()
+    # work-balanced rank slices (nnqs_chunk_work + balanced_bounds), 8 ranks
+    from paper_2306_16705_b200 import distributed as D
+    w = nnqs.nnqs_chunk_work(tab)
+    assert w.shape == ((n + 1023) // 1024,) and (w > 0).all()
+    assert np.array_equal(w, nnqs.nnqs_chunk_work(tab))
+    bs = [D.balanced_bounds(w, 8, r, n_rows=n) for r in range(8)]
+    assert bs[0][0] == 0 and bs[-1][1] == n and all(x[1] == y[0] for x, y in zip(bs[:-1], bs[1:]))
+    f = np.concatenate([nnqs.nnqs_local_energy(ham, tab, s0, n_rows=s1 - s0).cpu().numpy() for s0, s1 in bs])
+    assert a.tobytes() == f.tobytes()
 
 
 def test_c5_structured_equals_literal_hits(nnqs, dev, c5):
