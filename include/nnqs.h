@@ -160,7 +160,9 @@ int nnqs_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_
  *       stats_out[3] the folded terms evaluated.  E_loc of a row is
  *       bit-identical for any row_begin / n_rows slicing and across runs.
  *       The call synchronises its stream once (size of the entry-driven join)
- *       and uses a second, library-owned stream for that join.
+ *       and uses two library-owned streams, joined back into cuda_stream by
+ *       events before the call returns: one for that join, one for phase (ii)
+ *       (concurrent with phase (i); a row's summation order stays fixed).
  *       Every other call uses the literal loop.
  *   1 -- always the literal loop of Algorithm 2 (every row x every group,
  *       sector test, hash lookup of x').
