@@ -232,9 +232,10 @@ def nnqs_debug_counters(reset: bool = True):
 def nnqs_chunk_work(table: Table, chunk: int = REDUCE_CHUNK, stream=None):
     """Host int64[ceil(n/chunk)] work estimate per chunk of table rows (see include/nnqs.h)."""
     import numpy as np
-    out = np.zeros(max((table.n + chunk - 1) // chunk, 1), dtype=np.int64)
+    nch = (table.n + chunk - 1) // chunk if chunk > 0 else 0   # chunk <= 0: the library reports NNQS_E_ARG
+    out = np.zeros(max(nch, 1), dtype=np.int64)
     _check(_lib.nnqs_chunk_work(table.handle, int(chunk), out.ctypes.data, _stream(stream)))
-    return out[: (table.n + chunk - 1) // chunk]
+    return out[:nch]
 
 
 def nnqs_local_energy_check(eloc, stream=None):

@@ -411,6 +411,42 @@ def test_errors_and_edges(nnqs, dev):
     assert abs(got[0] - ref[0]) <= 1e-12 * abs(ref[0])
 
 
+def test_chunk_work_and_balanced_slices(nnqs, dev):
+    """nnqs_chunk_work: one positive estimate per 1024-row chunk (ragged tail
+    included), deterministic, rows-per-chunk on the literal path, NNQS_E_ARG on a
+    bad chunk; work-balanced slices of C4 evaluate bit-equal to one launch and
+    their chunk partials combine to the single-launch energy bit for bit."""
+    from paper_2306_16705_b200 import distributed as D
+    ham = ham_for(nnqs, 4)
+    st = C.sample_table(4, "full")
+    n = len(st.keys)
+    tab = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(st.logpsi, dev))
+    w = nnqs.nnqs_chunk_work(tab)
+    assert w.shape == ((n + 1023) // 1024,) and (w > 0).all()
+    assert np.array_equal(w, nnqs.nnqs_chunk_work(tab))
+    w256 = nnqs.nnqs_chunk_work(tab, chunk=256)
+    assert w256.shape == ((n + 255) // 256,) and w256.sum() == w.sum()
+    with pytest.raises(nnqs.NNQSError) as e:
+        nnqs.nnqs_chunk_work(tab, chunk=0)
+    assert e.value.code == nnqs.NNQS_E_ARG
+    nnqs.nnqs_set_algorithm(1)
+    try:
+        lit = nnqs.nnqs_chunk_work(tab)
+    finally:
+        nnqs.nnqs_set_algorithm(0)
+    assert lit.sum() == n and (lit[:-1] == 1024).all()
+    cnt = _t(st.counts, dev)
+    full = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n)
+    e1 = nnqs.nnqs_energy_combine(nnqs.nnqs_energy_chunk_partials(full, cnt), 1).cpu().numpy()
+    for world in (2, 3, 5):
+        bs = [D.balanced_bounds(w, world, r, n_rows=n) for r in range(world)]
+        parts = [nnqs.nnqs_local_energy(ham, tab, b, n_rows=e - b) for b, e in bs]
+        assert torch.cat(parts).cpu().numpy().tobytes() == full.cpu().numpy().tobytes()
+        p = torch.cat([nnqs.nnqs_energy_chunk_partials(x, cnt[b:e])[: (e - b + 1023) // 1024]
+                       for x, (b, e) in zip(parts, bs)])
+        assert nnqs.nnqs_energy_combine(p, 1).cpu().numpy().tobytes() == e1.tobytes()
+
+
 def test_tiny_amplitude_row_fallback(nnqs, dev):
     """A row with Re log psi(x) - s < -600 takes the per-term exp path (reading R11)."""
     m = C.molecule(3)
