@@ -303,7 +303,8 @@ def run_ours(args):
         tab = nnqs.nnqs_table_prepare(ham, 0, gk, gl, stream=stream)
         rb, re_ = b, e
         if world > 1:   # contiguous chunk-aligned slice of about equal estimated work
-            rb, re_ = D.balanced_bounds(nnqs.nnqs_chunk_work(tab, stream=stream), world, rank, n_rows=n)
+            wk, fl = nnqs.nnqs_chunk_work(tab, stream=stream, with_floor=True)
+            rb, re_ = D.balanced_bounds(wk, world, rank, n_rows=n, floor=fl)
             rows_of["b"], rows_of["e"] = rb, re_
         el = eloc[: re_ - rb]
         if timed:

@@ -188,11 +188,15 @@ int nnqs_debug_counters(uint64_t *out, int reset);
  * sorted table puts them together).  work_out: host i64[ceil(n/chunk)], chunk c
  * covering rows [c*chunk, min((c+1)*chunk, n)); relative units (list lengths
  * the row kernels scan, fixed costs for probed lists and join rows; the literal
- * Algorithm 2 path: rows per chunk).  Deterministic for a given table, so every
- * rank derives the same slices.  Synchronises cuda_stream.  NNQS_E_ARG on bad
- * arguments (chunk <= 0), NNQS_E_CUDA on a launch or copy failure.
+ * Algorithm 2 path: rows per chunk).  floor_out (NULL to skip): host
+ * i64[ceil(n/chunk)], in the same units, the largest single-row latency floor in
+ * the chunk (one warp evaluates one row: a row whose alpha and beta lists are
+ * both probed, the Hartree-Fock row, bounds its slice's time from below); 0 on
+ * the literal path.  Deterministic for a given table, so every rank derives the
+ * same slices.  Synchronises cuda_stream.  NNQS_E_ARG on bad arguments
+ * (chunk <= 0), NNQS_E_CUDA on a launch or copy failure.
  */
-int nnqs_chunk_work(nnqs_table t, int64_t chunk, int64_t *work_out, void *cuda_stream);
+int nnqs_chunk_work(nnqs_table t, int64_t chunk, int64_t *work_out, int64_t *floor_out, void *cuda_stream);
 
 /* Synchronises cuda_stream; NNQS_E_ZERO_PSI if any of eloc (device f64[n][2]) is NaN. */
 int nnqs_local_energy_check(const double *eloc, int64_t n, void *cuda_stream);

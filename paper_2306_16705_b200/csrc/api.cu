@@ -280,13 +280,16 @@ int nnqs_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_
     return nnqs_launch_local_energy(h, t, row_begin, rows, row_logpsi, n_rows, eloc_out, stats_out, cuda_stream);
 }
 
-int nnqs_chunk_work(nnqs_table t, int64_t chunk, int64_t *work_out, void *cuda_stream) {
+int nnqs_chunk_work(nnqs_table t, int64_t chunk, int64_t *work_out, int64_t *floor_out, void *cuda_stream) {
     if (!t || chunk <= 0 || (t->n > 0 && !work_out)) return nnqs_set_error(NNQS_E_ARG, "nnqs_chunk_work: bad arguments");
     DeviceGuard g(t->device);
     if (!g.ok) return nnqs_set_error(NNQS_E_CUDA, "cudaSetDevice failed");
-    if (t->spin_ready && g_algorithm != 1) return nnqs_chunk_work_spin(t, chunk, work_out, cuda_stream);
+    if (t->spin_ready && g_algorithm != 1) return nnqs_chunk_work_spin(t, chunk, work_out, floor_out, cuda_stream);
     const int64_t nch = (t->n + chunk - 1) / chunk;   // literal loop: every row costs K' pair tests
-    for (int64_t c = 0; c < nch; ++c) work_out[c] = std::min(chunk, t->n - c * chunk);
+    for (int64_t c = 0; c < nch; ++c) {
+        work_out[c] = std::min(chunk, t->n - c * chunk);
+        if (floor_out) floor_out[c] = 0;
+    }
     return NNQS_OK;
 }
 

@@ -160,7 +160,7 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream);
 void nnqs_table_release_spin(nnqs_table t);
 int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, int64_t n_rows,
                                   double *eloc, int64_t *stats, void *stream);
-int nnqs_chunk_work_spin(nnqs_table t, int64_t chunk, int64_t *work_host, void *stream);
+int nnqs_chunk_work_spin(nnqs_table t, int64_t chunk, int64_t *work_host, int64_t *floor_host, void *stream);
 int nnqs_algorithm();
 
 // device side (kernels.cu)

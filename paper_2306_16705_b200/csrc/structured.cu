@@ -1568,19 +1568,30 @@ __global__ void k_row_cost(TabSpin T, int64_t row_begin, int64_t n_rows, int32_t
 // (cost pd), rows of join-evaluated alpha groups cost pj.  One block per chunk.
 __global__ void __launch_bounds__(256) k_chunk_work(TabSpin T, int64_t chunk, int32_t thr_d, int32_t thr_rowheavy,
                                                     const int32_t *nl_cost, int32_t w0, int32_t pd, int32_t pj,
-                                                    long long *work) {
+                                                    int32_t px, int32_t pf, long long *work, long long *floor_out) {
     const int64_t r0 = (int64_t)blockIdx.x * chunk;
     const int64_t r1 = (r0 + chunk < T.n) ? r0 + chunk : T.n;
-    long long w = 0;
+    long long w = 0, fl = 0;
     for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
         const int32_t ga = T.ga_of[i], gb = T.gb_of[i];
         const int32_t la = T.offA[ga + 1] - T.offA[ga], lb = T.offB[gb + 1] - T.offB[gb];
         w += w0 + (lb > thr_d ? pd : lb) + (la > thr_d ? pd : la) + (la > thr_rowheavy ? pj : (nl_cost ? nl_cost[ga] : 0));
+        // rows whose alpha and beta lists are both probed (the Hartree-Fock row and its
+        // like) drain matches near both strings in one warp: ~ la * lb / n, a latency floor
+        if (la > thr_d && lb > thr_d) {
+            w += (long long)px * la * lb / T.n;
+            fl = max(fl, (long long)pf * la * lb / T.n);
+        }
     }
     typedef cub::BlockReduce<long long, 256> Red;
     __shared__ typename Red::TempStorage tmp;
     const long long tot = Red(tmp).Sum(w);
-    if (threadIdx.x == 0) work[blockIdx.x] = tot;
+    __syncthreads();
+    const long long mx = Red(tmp).Reduce(fl, cub::Max());
+    if (threadIdx.x == 0) {
+        work[blockIdx.x] = tot;
+        if (floor_out) floor_out[blockIdx.x] = mx;
+    }
 }
 
 __global__ void k_find_heavy(const int32_t *listA_idx, const int32_t *ga_of, const int32_t *offA, int64_t n,
@@ -2287,16 +2298,19 @@ void nnqs_table_release_spin(nnqs_table t) {
     t->spin_ready = false;
 }
 
-int nnqs_chunk_work_spin(nnqs_table t, int64_t chunk, int64_t *work_host, void *stream) {
+int nnqs_chunk_work_spin(nnqs_table t, int64_t chunk, int64_t *work_host, int64_t *floor_host, void *stream) {
     const int64_t nch = (t->n + chunk - 1) / chunk;
     if (nch == 0) return NNQS_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    static int w0 = -1, pd = -1, pj = -1;   // estimate weights (measurement knobs: NNQS_WORK_W0/PD/PJ)
+    static int w0 = -1, pd = -1, pj = -1, px = -1, pf = -1;   // estimate weights (knobs: NNQS_WORK_*)
     if (w0 < 0) {
         const char *a = std::getenv("NNQS_WORK_W0"), *b = std::getenv("NNQS_WORK_PD"), *c = std::getenv("NNQS_WORK_PJ");
+        const char *d = std::getenv("NNQS_WORK_PX"), *f = std::getenv("NNQS_WORK_PF");
+        pf = f ? std::atoi(f) : 32768;
         w0 = a ? std::atoi(a) : 256;
         pd = b ? std::atoi(b) : 4096;
         pj = c ? std::atoi(c) : 4096;
+        px = d ? std::atoi(d) : 0;
     }
     TabSpin tv{};
     tv.n = t->n;
@@ -2305,10 +2319,13 @@ int nnqs_chunk_work_spin(nnqs_table t, int64_t chunk, int64_t *work_host, void *
     tv.offA = t->offA;
     tv.offB = t->offB;
     long long *wd = nullptr;
-    int rc = cuda_check(cudaMallocAsync((void **)&wd, 8 * nch, st), "alloc chunk work");
+    int rc = cuda_check(cudaMallocAsync((void **)&wd, 16 * nch, st), "alloc chunk work");
     if (rc) return rc;
-    k_chunk_work<<<(unsigned)nch, 256, 0, st>>>(tv, chunk, t->thr_double, t->thr_rowheavy, t->nl_cost, w0, pd, pj, wd);
+    k_chunk_work<<<(unsigned)nch, 256, 0, st>>>(tv, chunk, t->thr_double, t->thr_rowheavy, t->nl_cost, w0, pd, pj, px,
+                                                pf, wd, wd + nch);
     rc = cuda_check(cudaMemcpyAsync(work_host, wd, 8 * nch, cudaMemcpyDeviceToHost, st), "read chunk work");
+    if (!rc && floor_host)
+        rc = cuda_check(cudaMemcpyAsync(floor_host, wd + nch, 8 * nch, cudaMemcpyDeviceToHost, st), "read chunk floor");
     cudaFreeAsync(wd, st);
     if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync chunk work");
     return rc;

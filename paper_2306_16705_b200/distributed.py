@@ -30,16 +30,61 @@ def shard_bounds(n_rows: int, world: int, rank: int, chunk: int = REDUCE_CHUNK):
     return min(lo * chunk, n_rows), min(hi * chunk, n_rows)
 
 
-def balanced_bounds(work, world: int, rank: int, chunk: int = REDUCE_CHUNK, n_rows: int | None = None):
+def balanced_bounds(work, world: int, rank: int, chunk: int = REDUCE_CHUNK, n_rows: int | None = None,
+                    floor=None):
     """Contiguous, chunk-aligned slice [begin, end) of the table rows for this rank
     with about equal estimated work (nnqs_chunk_work: one int64 per chunk): rank r
-    starts at the first chunk whose work prefix reaches r/world of the total.  Pure
-    integer arithmetic on the replicated estimate, so every rank derives the same
-    slices; chunk alignment keeps the energy bit-identical to 1 GPU."""
+    starts at the first chunk whose work prefix reaches r/world of the total.  With
+    `floor` (nnqs_chunk_work's per-chunk single-row latency floor) a slice costs
+    max(its largest floor, its work) and the slices minimise the largest cost
+    (bisection on the bound, then a greedy fill from the left).  Pure integer
+    arithmetic on the replicated estimate, so every rank derives the same slices;
+    chunk alignment keeps the energy bit-identical to 1 GPU."""
     w = [int(v) for v in work]
     n_chunks = len(w)
     n = n_chunks * chunk if n_rows is None else n_rows
     total = sum(w)
+    if floor is not None and n_chunks and max(int(v) for v in floor) > 0:
+        fl = [int(v) for v in floor]
+
+        def cost(acc, mf):   # a slice's time: its work, or its slowest row plus half its work
+            return max(acc, mf + acc // 2)
+
+        def feasible(bound):
+            k, acc, mf = 1, 0, 0
+            for c in range(n_chunks):
+                if cost(w[c], fl[c]) > bound:
+                    return False
+                if cost(acc + w[c], max(mf, fl[c])) > bound:
+                    k, acc, mf = k + 1, 0, 0
+                    if k > world:
+                        return False
+                acc += w[c]
+                mf = max(mf, fl[c])
+            return True
+
+        lo, hi = 0, max(total, max(fl)) + total
+        while lo < hi:
+            mid = (lo + hi) // 2
+            if feasible(mid):
+                hi = mid
+            else:
+                lo = mid + 1
+        # balanced fill: each rank takes at most its fair share of the remaining work
+        # and stays within the optimal bound; the last rank takes the rest
+        st, c, rem = [0], 0, total
+        for r in range(world - 1):
+            R = world - r
+            acc, mf = 0, 0
+            while c < n_chunks:
+                nacc, nmf = acc + w[c], max(mf, fl[c])
+                if acc + mf > 0 and (nacc * R > rem + R - 1 or cost(nacc, nmf) > lo):
+                    break
+                acc, mf, c = nacc, nmf, c + 1
+            rem -= acc
+            st.append(c)
+        st.append(n_chunks)
+        return min(st[rank] * chunk, n), min(st[rank + 1] * chunk, n) if rank + 1 < world else n
     if total <= 0:
         return shard_bounds(n, world, rank, chunk)
 

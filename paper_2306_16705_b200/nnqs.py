@@ -35,7 +35,7 @@ _sig = {
     "nnqs_table_info": ([P, P, P, P], ctypes.c_int),
     "nnqs_local_energy": ([P, P, I64, P, P, I64, P, P, P], ctypes.c_int),
     "nnqs_local_energy_check": ([P, I64, P], ctypes.c_int),
-    "nnqs_chunk_work": ([P, I64, P, P], ctypes.c_int),
+    "nnqs_chunk_work": ([P, I64, P, P, P], ctypes.c_int),
     "nnqs_set_algorithm": ([ctypes.c_int], ctypes.c_int),
     "nnqs_get_algorithm": ([], ctypes.c_int),
     "nnqs_debug_counters": ([P, ctypes.c_int], ctypes.c_int),
@@ -229,13 +229,16 @@ def nnqs_debug_counters(reset: bool = True):
     return out
 
 
-def nnqs_chunk_work(table: Table, chunk: int = REDUCE_CHUNK, stream=None):
-    """Host int64[ceil(n/chunk)] work estimate per chunk of table rows (see include/nnqs.h)."""
+def nnqs_chunk_work(table: Table, chunk: int = REDUCE_CHUNK, stream=None, with_floor: bool = False):
+    """Host int64[ceil(n/chunk)] work estimate per chunk of table rows (see include/nnqs.h);
+    with_floor: (work, floor), floor = the largest single-row latency floor per chunk."""
     import numpy as np
     nch = (table.n + chunk - 1) // chunk if chunk > 0 else 0   # chunk <= 0: the library reports NNQS_E_ARG
     out = np.zeros(max(nch, 1), dtype=np.int64)
-    _check(_lib.nnqs_chunk_work(table.handle, int(chunk), out.ctypes.data, _stream(stream)))
-    return out[:nch]
+    fl = np.zeros(max(nch, 1), dtype=np.int64)
+    _check(_lib.nnqs_chunk_work(table.handle, int(chunk), out.ctypes.data, fl.ctypes.data if with_floor else None,
+                                _stream(stream)))
+    return (out[:nch], fl[:nch]) if with_floor else out[:nch]
 
 
 def nnqs_local_energy_check(eloc, stream=None):

@@ -27,7 +27,7 @@ from synth import configs as C
 
 c = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-split = sys.argv[3] if len(sys.argv) > 3 else "work"   # "work": balanced_bounds, "count": shard_bounds
+split = sys.argv[3] if len(sys.argv) > 3 else "work"   # "work" (with floors), "work_nofloor", "count"
 NVLINK_GBS = 900.0          # per-direction NVLink 5 bandwidth per GPU (B200_PROFILING.md)
 dev = torch.device("cuda", 0)
 m = C.molecule(c)
@@ -68,12 +68,16 @@ def rank_step(b, e):
 
 
 tab0 = nnqs.nnqs_table_prepare(ham, 0, keys, lp, stream=stream)
-work = nnqs.nnqs_chunk_work(tab0, stream=stream)
+work, floor = nnqs.nnqs_chunk_work(tab0, stream=stream, with_floor=True)
 tab0.close()
 
 
 def bounds(P, r):
-    return D.balanced_bounds(work, P, r, n_rows=n) if split == "work" else D.shard_bounds(n, P, r)
+    if split == "work":
+        return D.balanced_bounds(work, P, r, n_rows=n, floor=floor)
+    if split == "work_nofloor":
+        return D.balanced_bounds(work, P, r, n_rows=n)
+    return D.shard_bounds(n, P, r)
 
 
 res = {"what": "per-rank step times of the P-GPU bench flow, each rank measured alone on one B200",

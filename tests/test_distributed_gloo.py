@@ -123,6 +123,30 @@ def test_balanced_bounds_cover_align_balance():
                         assert w * world <= tot + world * int(work.max())
 
 
+def test_balanced_bounds_with_floor():
+    """Floor-aware slices: cover, chunk-aligned, the chunk with the slow row gets a short
+    slice at large world sizes, and no slice is costlier than the even split's worst."""
+    n = 100 * 1024 - 5
+    w = np.full(100, 10, dtype=np.int64)
+    fl = np.zeros(100, dtype=np.int64)
+    fl[0] = 300
+
+    def cost(b, e):
+        c0, c1 = b // 1024, (e + 1023) // 1024
+        acc, mf = int(w[c0:c1].sum()), int(fl[c0:c1].max(initial=0))
+        return max(acc, mf + acc // 2)
+
+    for world in (1, 2, 3, 4, 8):
+        bs = [D.balanced_bounds(w, world, r, n_rows=n, floor=fl) for r in range(world)]
+        assert bs[0][0] == 0 and bs[-1][1] == n
+        assert all(x[1] == y[0] and (y[0] % 1024 == 0 or y[0] == n) for x, y in zip(bs[:-1], bs[1:]))
+        plain = [D.balanced_bounds(w, world, r, n_rows=n) for r in range(world)]
+        assert max(cost(b, e) for b, e in bs) <= max(cost(b, e) for b, e in plain)
+    bs8 = [D.balanced_bounds(w, 8, r, n_rows=n, floor=fl) for r in range(8)]
+    assert bs8[0] == (0, 1024)
+    assert D.balanced_bounds(w, 4, 1, n_rows=n, floor=np.zeros(100, np.int64)) == D.balanced_bounds(w, 4, 1, n_rows=n)
+
+
 def test_shard_bounds_cover_and_align():
     for n in (0, 1, 1023, 1024, 10 * 1024 + 77, 10**6):
         for world in (1, 2, 3, 4, 8):
