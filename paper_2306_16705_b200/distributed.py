@@ -44,7 +44,8 @@ def balanced_bounds(work, world: int, rank: int, chunk: int = REDUCE_CHUNK, n_ro
     n_chunks = len(w)
     n = n_chunks * chunk if n_rows is None else n_rows
     total = sum(w)
-    if floor is not None and n_chunks and max(int(v) for v in floor) > 0:
+    # floors at most half a fair share never bind (floor + work/2 <= work): the plain split
+    if floor is not None and n_chunks and 2 * world * max(int(v) for v in floor) > total:
         fl = [int(v) for v in floor]
 
         def cost(acc, mf):   # a slice's time: its work, or its slowest row plus half its work

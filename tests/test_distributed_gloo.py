@@ -145,6 +145,10 @@ def test_balanced_bounds_with_floor():
     bs8 = [D.balanced_bounds(w, 8, r, n_rows=n, floor=fl) for r in range(8)]
     assert bs8[0] == (0, 1024)
     assert D.balanced_bounds(w, 4, 1, n_rows=n, floor=np.zeros(100, np.int64)) == D.balanced_bounds(w, 4, 1, n_rows=n)
+    small = np.zeros(100, np.int64)
+    small[0] = 1000 // (2 * 4)                   # half a fair share at world 4: the plain split
+    assert [D.balanced_bounds(w, 4, r, n_rows=n, floor=small) for r in range(4)] == \
+        [D.balanced_bounds(w, 4, r, n_rows=n) for r in range(4)]
 
 
 def test_shard_bounds_cover_and_align():
