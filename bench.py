@@ -171,9 +171,10 @@ def profile_traffic():
             "ncu_alu_pipe_pct_time_weighted": (alu_w / t_w) if t_w else None, "ncu_alu_pipe_pct": per}
 
 
-def cpu_baseline(mol, st, n_rows_req, seconds_target=15.0):
+def cpu_baseline(mol, st, n_rows_req, eloc_gpu=None, seconds_target=15.0):
     """The oracle (as it stands) on a bounded, seeded sample of this workload's
-    rows, on all host cores."""
+    rows, on all host cores -- and, since it computes them anyway, those rows'
+    E_loc compared with the GPU's of the same run (reading R14 tolerance)."""
     import numpy as np
     from oracle import rows as R
     from synth import configs as C
@@ -185,11 +186,20 @@ def cpu_baseline(mol, st, n_rows_req, seconds_target=15.0):
     n = n_rows_req or int(max(16, min(20000, seconds_target / max(per_row, 1e-6))))
     idx = C.oracle_row_subset(5 if mol.n_qubits == 120 else 4, len(st.keys), n)
     t0 = time.perf_counter()
-    R.eloc(mol.h1, mol.h2, mol.e_core, st.keys[idx], st.logpsi[idx], keys=st.keys, logpsi=st.logpsi)
+    ref, scale = R.eloc(mol.h1, mol.h2, mol.e_core, st.keys[idx], st.logpsi[idx], keys=st.keys, logpsi=st.logpsi,
+                        with_scale=True)
     dt = time.perf_counter() - t0
-    return {"value": len(idx) / dt, "unit": UNIT, "cores": R.num_threads(), "kind": "oracle",
-            "sample": f"{len(idx)} seeded rows (seed 705) of the {len(st.keys)}-row table, full sample-aware "
-                      f"E_loc per row (plain term-by-term Eq. 9 + bisection), {dt:.1f} s"}
+    out = {"value": len(idx) / dt, "unit": UNIT, "cores": R.num_threads(), "kind": "oracle",
+           "sample": f"{len(idx)} seeded rows (seed 705) of the {len(st.keys)}-row table, full sample-aware "
+                     f"E_loc per row (plain term-by-term Eq. 9 + bisection), {dt:.1f} s"}
+    if eloc_gpu is not None:
+        got = eloc_gpu[idx, 0] + 1j * eloc_gpu[idx, 1]
+        err = np.abs(got - ref) / scale
+        out["parity"] = {"rows": int(len(idx)), "max_err_over_scale": float(err.max()), "tol": 1e-10,
+                         "ok": bool((err <= 1e-10).all()),
+                         "what": "GPU E_loc of the timed run vs these oracle rows, |dE| / sum |H psi'/psi| "
+                                 "(DESIGN.md R14)"}
+    return out
 
 
 def count_launches(step_fn):
@@ -290,6 +300,7 @@ def run_ours(args):
     n_local = e - b
     stream = torch.cuda.current_stream()
     eloc = torch.empty((n if world > 1 else n_local, 2), dtype=torch.float64, device=dev)
+    part1 = torch.empty(((n + 1023) // 1024 + 1, 3), dtype=torch.float64, device=dev)
     rows_of = {"b": b, "e": e}   # rows this rank evaluates (world > 1: work-balanced, per step)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ev_k = []          # (start, end) events around nnqs_local_energy
@@ -311,15 +322,18 @@ def run_ours(args):
             s0 = torch.cuda.Event(enable_timing=True)
             s1 = torch.cuda.Event(enable_timing=True)
             s0.record(stream)
-        nnqs.nnqs_local_energy(ham, tab, rb, n_rows=re_ - rb, eloc_out=el, stream=stream)
+        cnt_rows = gc[rb:re_] if world > 1 else cd
+        p1 = part1[: (re_ - rb + 1023) // 1024]
+        # E_loc of the slice + the fused first pass of Eq. (6) per 1024-row chunk
+        nnqs.nnqs_local_energy(ham, tab, rb, n_rows=re_ - rb, eloc_out=el, counts=cnt_rows, partials_out=p1,
+                               stream=stream)
         if timed:
             s1.record(stream)
             ev_k.append((s0, s1))
         if world > 1:
-            en = D.distributed_energy(el, gc[rb:re_], stream=stream)
+            en = D.distributed_energy(el, cnt_rows, stream=stream, p1=p1)
         else:
-            part = nnqs.nnqs_energy_chunk_partials(eloc, cd, stream=stream)
-            m1 = nnqs.nnqs_energy_combine(part, 1, stream=stream)
+            m1 = nnqs.nnqs_energy_combine(p1, 1, stream=stream)
             part2 = nnqs.nnqs_energy_chunk_partials(eloc, cd, mean_dev=m1[:2].contiguous(), stream=stream)
             m2 = nnqs.nnqs_energy_combine(part2, 2, stream=stream)
             en = torch.stack([m1[0], m1[1], m2[0], m1[2]])
@@ -410,12 +424,12 @@ def run_ours(args):
     clk_sum = clk.summary()
     sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
     alu_peak, alu_src = alu_peak_ops(sm_mhz)
-    # Algorithmic integer work of one local-energy launch (rank 0's slice), from
-    # the kernel's own counters: every examined candidate
-    # (list entry, multimap probe, alpha-single test) needs >= 4 32-bit ops
-    # (64-bit XOR = 2 LOP3, 64-bit popcount test = 2), every evaluated Pauli
-    # string >= 6 (128-bit AND = 4 LOP3, parity add, sign-bit LOP3).
-    r0 = D.shard_bounds(n, world, 0)
+    # Algorithmic integer work of one local-energy launch, from the kernels' own
+    # counters summed over ranks and divided by the rank count (a per-rank average)
+    # (DESIGN.md 'Roofline'): every examined candidate (list entry, multimap probe,
+    # alpha-single test) needs >= 4 32-bit ops (64-bit XOR = 2 LOP3, 64-bit popcount
+    # test = 2), every evaluated Pauli string >= 6 (128-bit AND = 4 LOP3, parity add,
+    # sign-bit LOP3).
     ops_launch = 4 * int(st_local[1]) + 6 * int(st_local[3])
     if world > 1:
         ops_launch = ops_launch // world
@@ -473,9 +487,14 @@ def run_ours(args):
         "launches_per_step": launch_names,
         "algorithm": "structured (alpha/beta-factorised; identical hit set to Algorithm 2's loop)",
     }
+    parity_ok = True
     if not args.no_cpu_baseline and world == 1:
-        out["cpu_baseline"] = cpu_baseline(mol, st, args.cpu_rows)
+        out["cpu_baseline"] = cpu_baseline(mol, st, args.cpu_rows, eloc_gpu=eloc.cpu().numpy())
+        parity_ok = out["cpu_baseline"].get("parity", {}).get("ok", True)
     print(json.dumps(out), flush=True)
+    if not parity_ok:
+        print("bench: GPU E_loc disagrees with the oracle rows (see cpu_baseline.parity)", file=sys.stderr)
+        sys.exit(3)
     if world > 1:
         dist.destroy_process_group()
 

@@ -110,19 +110,68 @@ int nnqs_ham_export(nnqs_ham h, uint64_t *xmask, int64_t *offsets, uint64_t *zma
 int nnqs_ham_free(nnqs_ham h);
 
 /*
+ * Per-table options (no process-wide state: every knob lives in the table).
+ *   algorithm    0 (NNQS_ALGO_AUTO): table rows (rows == NULL) of a sample-aware
+ *                table over a Hamiltonian from nnqs_ham_compress use the
+ *                alpha/beta-factorised enumeration (DESIGN.md "structured
+ *                path"): the same (row, group) pairs with x' in the table as
+ *                the literal loop, found by scanning the table's alpha-/beta-
+ *                string lists and probing a deletion-key multimap for heavy
+ *                strings; H_xx' is the group's Pauli sum on the in-sector folded
+ *                table (R21; diagonal and single-excitation groups in
+ *                occupation form, R22), so E_loc agrees with the literal loop to
+ *                rounding (R14), not bit for bit.  Every other call (explicit
+ *                rows, exact mode, nnqs_ham_from_pauli tables) uses the literal
+ *                loop.  1 (NNQS_ALGO_LITERAL): always the literal loop of
+ *                Algorithm 2 (every row x every group, sector test, hash lookup).
+ *   thr_single   structured path: adjacent alpha strings with more table rows
+ *                than this are probed through the deletion multimap instead of
+ *                scanned (0 = default 128)
+ *   thr_double   same-spin lists longer than this are probed (0 = default 8192)
+ *   thr_rowheavy alpha groups with more rows than this take phase (iii) through
+ *                the entry-driven join (0 = default 16384; raised to thr_single)
+ * The thresholds change the work split, never the hit set or a row's value
+ * beyond rounding order.  nnqs_options_default fills the defaults.
+ */
+#define NNQS_ALGO_AUTO 0
+#define NNQS_ALGO_LITERAL 1
+typedef struct {
+    int32_t algorithm;
+    int32_t thr_single;
+    int32_t thr_double;
+    int32_t thr_rowheavy;
+    int32_t reserved[12];   /* must be zero */
+} nnqs_options;
+void nnqs_options_default(nnqs_options *opt);
+
+/*
  * nnqs_table_prepare -- the lookup tables of Algorithm 2 (id_lut / wf_lut,
  * P:383): validates strict 128-bit order, builds psi_hat(y) =
  * exp(logpsi(y) - s), s = max Re logpsi, and a GF(2)-linear hash index over the
- * keys (the lookup that replaces binary_find).
+ * keys (the lookup that replaces binary_find); sample-aware tables over a
+ * spin-conserving Hamiltonian also get the alpha/beta string index of the
+ * structured path (CSR by alpha / beta string, adjacent-alpha lists, deletion
+ * multimap).
  *   mode 0 (sample-aware): keys device u64[n][2] (sorted), logpsi device f64[n][2]
  *   mode 1 (exact): keys == NULL, n = 2^N (N <= 30), logpsi indexed by configuration
- *   cuda_stream  cudaStream_t (NULL = legacy default stream)
- * Stream-ordered; returns NNQS_E_TABLE (after a stream sync) if the order check
- * fails.
+ *   opt          NULL = defaults (nnqs_options_default)
+ *   cuda_stream  cudaStream_t (NULL = legacy default stream); keys / logpsi are
+ *                read in stream order; the table copies what it keeps.
+ * The table owns its device memory and two private CUDA streams (used inside
+ * nnqs_local_energy, joined back by events).  It records an event after every
+ * call that uses it; nnqs_table_free orders the release after that event on a
+ * private stream, so the caller's streams need not outlive the table.  A table
+ * may be used by one call at a time (calls on one thread, or serialised).
+ * Synchronises cuda_stream (table sizes); returns NNQS_E_TABLE if the order
+ * check fails, NNQS_E_NOMEM / NNQS_E_CUDA on device errors (nothing leaks).
  */
 int nnqs_table_prepare(nnqs_ham h, int mode, const uint64_t *keys, const double *logpsi,
                        int64_t n, void *cuda_stream, nnqs_table *out);
+int nnqs_table_prepare_ex(nnqs_ham h, int mode, const uint64_t *keys, const double *logpsi,
+                          int64_t n, const nnqs_options *opt, void *cuda_stream, nnqs_table *out);
 int nnqs_table_free(nnqs_table t);
+/* the table's algorithm (NNQS_ALGO_*); not concurrently with a call using t */
+int nnqs_table_set_algorithm(nnqs_table t, int algorithm);
 /* table size and the log-psi shift s (host out; may be NULL) */
 int nnqs_table_info(nnqs_table t, int64_t *n, double *shift, int64_t *device_bytes);
 
@@ -134,41 +183,32 @@ int nnqs_table_info(nnqs_table t, int64_t *n, double *shift, int64_t *device_byt
  *   rows != NULL: explicit device u64[n_rows][2] with row_logpsi device
  *                 f64[n_rows][2] (any configurations).
  *   eloc_out  device f64[n_rows][2] = (Re, Im) E_loc
+ *   counts, partials_out  optional (both or neither): counts device i64[n_rows]
+ *             (sample weights w); partials_out device
+ *             f64[ceil(n_rows/NNQS_REDUCE_CHUNK)][3] receives the first pass of
+ *             Eq. (6) per chunk of NNQS_REDUCE_CHUNK rows of this call, (W,
+ *             sum w Re E, sum w Im E), fused into the E_loc epilogue: the warp
+ *             that completes a chunk's last row reduces the chunk in the fixed
+ *             order of nnqs_energy_chunk_partials (bit-identical to it), so
+ *             chunk-aligned rank slices combine bit for bit (stage 4).
  *   stats_out optional device i64[4] (zeroed by the caller) accumulating
  *             (row-group pairs, pairs whose x' shares x's particle sector,
- *              lookups that hit, Pauli strings evaluated); NULL to skip
+ *              lookups that hit, Pauli strings evaluated); NULL to skip.  On the
+ *             structured path stats_out[0] is R x K' by definition (the pairs
+ *             the enumeration resolves, not a counter), stats_out[1] counts
+ *             list entries / probes examined and stats_out[3] folded terms.
  * x' absent from the table contributes zero.  For Hamiltonians from
  * nnqs_ham_compress, groups whose x' leaves x's (N_alpha, N_beta) sector are
  * skipped (their exact H_xx' is 0).  A row with psi(x) = 0 gets NaN; this is
- * reported by nnqs_local_energy_check().  Asynchronous on cuda_stream.
+ * reported by nnqs_local_energy_check().  Asynchronous on cuda_stream, except
+ * that the structured path synchronises once (size of its entry-driven join).
+ * E_loc of a row is bit-identical for any row_begin / n_rows slicing, across
+ * runs, and (structured path) independent of the row schedule.
  */
 int nnqs_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_t *rows,
                       const double *row_logpsi, int64_t n_rows, double *eloc_out,
-                      int64_t *stats_out, void *cuda_stream);
-
-/*
- * Algorithm selection (process-wide):
- *   0 (default) -- rows == NULL in sample-aware mode with a Hamiltonian from
- *       nnqs_ham_compress: the alpha/beta-factorised enumeration (DESIGN.md
- *       "structured path"): the same (row, group) pairs with x' in the table
- *       as the literal loop, found by scanning the table's alpha-/beta-string
- *       lists and probing a deletion-key multimap for heavy strings; H_xx' is
- *       the group's Pauli sum on the in-sector folded table (R21;
- *       diagonal and single-excitation groups in occupation form, R22), so
- *       E_loc agrees with the literal loop to rounding (R14), not bit for bit.
- *       stats_out[1] then counts list entries / probes examined and
- *       stats_out[3] the folded terms evaluated.  E_loc of a row is
- *       bit-identical for any row_begin / n_rows slicing and across runs.
- *       The call synchronises its stream once (size of the entry-driven join)
- *       and uses two library-owned streams, joined back into cuda_stream by
- *       events before the call returns: one for that join, one for phase (ii)
- *       (concurrent with phase (i); a row's summation order stays fixed).
- *       Every other call uses the literal loop.
- *   1 -- always the literal loop of Algorithm 2 (every row x every group,
- *       sector test, hash lookup of x').
- */
-int nnqs_set_algorithm(int algorithm);
-int nnqs_get_algorithm(void);
+                      const int64_t *counts, double *partials_out, int64_t *stats_out,
+                      void *cuda_stream);
 
 /*
  * Profiling aid (not part of the method): cycle counters of the structured
@@ -242,13 +282,32 @@ int nnqs_grad_weights(const double *eloc, const int64_t *counts, int64_t n, cons
 
 /*
  * Parity/debug (small inputs): every (row, group) whose x' = x ^ X_k is found
- * in the table, with its index and H_xx'.  rows: host u64[n_rows][2].  Outputs
- * host arrays of capacity max_pairs; n_pairs_out = number found (may exceed
- * max_pairs, then NNQS_E_SIZE).  Order unspecified.
+ * in the table, with its index and H_xx', by the literal loop (Algorithm 2,
+ * P:399-418).  rows: host u64[n_rows][2].  Outputs host arrays of capacity
+ * max_pairs; n_pairs_out = number found (may exceed max_pairs, then
+ * NNQS_E_SIZE).  Order unspecified.
  */
 int nnqs_coupled_debug(nnqs_ham h, nnqs_table t, const uint64_t *rows_host, int64_t n_rows,
                        int64_t max_pairs, int64_t *row_id, int64_t *group_id, uint64_t *xprime,
                        int64_t *table_idx, double *h_xxp, int64_t *n_pairs_out);
+
+/*
+ * Parity/debug of the production path (P3 of DESIGN.md Sec. 4): runs exactly
+ * the launch sequence nnqs_local_energy uses for the table rows
+ * [row_begin, row_begin + n_rows) (the table's algorithm; the structured
+ * kernels with their multimap probes, entry-driven join and occupation forms)
+ * with a hit log enabled, and returns every hit those kernels evaluate:
+ * row_id = table index of the row, table_idx = table index of x' (the lookup
+ * index), xprime = the key of x' (read from the table), group_id = k with
+ * X_k = x ^ x' (host search of the grouped table, -1 if X is not a group),
+ * h_xxp = the H_xx' the kernel multiplied with psi(x') (the diagonal x' = x
+ * included).  Host outputs of capacity max_pairs (any may be NULL);
+ * n_pairs_out = hits found (> max_pairs: NNQS_E_SIZE, the first max_pairs in
+ * unspecified order are written).  Synchronises; for tests on small slices.
+ */
+int nnqs_coupled_debug_rows(nnqs_ham h, nnqs_table t, int64_t row_begin, int64_t n_rows, int64_t max_pairs,
+                            int64_t *row_id, int64_t *group_id, uint64_t *xprime, int64_t *table_idx,
+                            double *h_xxp, int64_t *n_pairs_out);
 
 #ifdef __cplusplus
 }

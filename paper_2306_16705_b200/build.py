@@ -13,7 +13,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 def sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
-                  if f.endswith((".cu", ".cpp", ".h")))
+                  if f.endswith((".cu", ".cpp", ".h", ".cuh")))
 
 
 def needs_build() -> bool:
@@ -31,7 +31,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for src in sources():
-        if src.endswith(".h"):
+        if src.endswith((".h", ".cuh")):
             continue
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         if src.endswith(".cu"):

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 
@@ -26,16 +27,28 @@ struct DeviceGuard {
     }
 };
 
-bool g_pool_configured[64] = {false};
+// The library's own stream-ordered memory pool, one per device, created once
+// (thread-safe).  Its release threshold keeps freed blocks for reuse by the next
+// call (the per-call scratch is large and the call repeats every VMC step); the
+// device's default pool -- shared with PyTorch / NCCL -- is not touched.
+std::once_flag g_pool_once[64];
+cudaMemPool_t g_pool[64] = {};
 
-void configure_pool(int device) {
-    if (device < 0 || device >= 64 || g_pool_configured[device]) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    g_pool_configured[device] = true;
+cudaMemPool_t library_pool(int device) {
+    if (device < 0 || device >= 64) return nullptr;
+    std::call_once(g_pool_once[device], [device]() {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        cudaMemPool_t pool = nullptr;
+        if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            g_pool[device] = pool;
+        }
+    });
+    return g_pool[device];
 }
 
 int check_symmetry(const double *h1, const double *h2, int n) {
@@ -67,8 +80,6 @@ int check_symmetry(const double *h1, const double *h2, int n) {
     return NNQS_OK;
 }
 
-int g_algorithm = 0;
-
 int finish_ham(nnqs_ham h, int device, nnqs_ham *out) {
     h->device = device;
     nnqs_spin_index_build(h->host, h->spin);
@@ -80,7 +91,6 @@ int finish_ham(nnqs_ham h, int device, nnqs_ham *out) {
     }
     DeviceGuard g(device);
     if (!g.ok) return nnqs_set_error(NNQS_E_CUDA, "cudaSetDevice failed");
-    configure_pool(device);
     int rc = nnqs_ham_upload(h);
     if (!rc) rc = nnqs_spin_index_upload(h);
     if (rc) {
@@ -93,7 +103,14 @@ int finish_ham(nnqs_ham h, int device, nnqs_ham *out) {
 }
 }  // namespace
 
-int nnqs_algorithm() { return g_algorithm; }
+cudaError_t nnqs_malloc_async(void **p, size_t bytes, cudaStream_t st) {
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    cudaMemPool_t pool = library_pool(dev);
+    if (!pool) return cudaMallocAsync(p, bytes, st);   // pool creation failed: the default pool
+    return cudaMallocFromPoolAsync(p, bytes, pool, st);
+}
 
 int nnqs_set_error(int code, const std::string &msg) {
     g_last_error = msg;
@@ -194,12 +211,41 @@ int nnqs_ham_free(nnqs_ham h) {
     return NNQS_OK;
 }
 
+void nnqs_options_default(nnqs_options *opt) {
+    if (!opt) return;
+    std::memset(opt, 0, sizeof(*opt));
+    opt->algorithm = NNQS_ALGO_AUTO;
+    opt->thr_single = 128;     // measured (step ms): 96 63.52, 128 63.45, 192 63.67, 256 64.15
+    opt->thr_double = 8192;    // measured (step ms): 2048 69.46, 4096 63.51, 8192 63.15
+    opt->thr_rowheavy = 16384; // DESIGN.md Sec. 7 (entry-driven join below 16384 rows: slower)
+}
+
 int nnqs_table_prepare(nnqs_ham h, int mode, const uint64_t *keys, const double *logpsi, int64_t n,
                        void *cuda_stream, nnqs_table *out) {
+    return nnqs_table_prepare_ex(h, mode, keys, logpsi, n, nullptr, cuda_stream, out);
+}
+
+int nnqs_table_prepare_ex(nnqs_ham h, int mode, const uint64_t *keys, const double *logpsi, int64_t n,
+                          const nnqs_options *opt, void *cuda_stream, nnqs_table *out) {
     if (!h || !out || n < 0 || (mode != 0 && mode != 1) || (n > 0 && !logpsi))
         return nnqs_set_error(NNQS_E_ARG, "nnqs_table_prepare: bad arguments");
     if (h->device < 0) return nnqs_set_error(NNQS_E_ARG, "host-only Hamiltonian (device < 0)");
     *out = nullptr;
+    nnqs_options o;
+    nnqs_options_default(&o);
+    if (opt) {
+        for (int32_t r : opt->reserved)
+            if (r) return nnqs_set_error(NNQS_E_ARG, "nnqs_options.reserved must be zero");
+        if (opt->algorithm != NNQS_ALGO_AUTO && opt->algorithm != NNQS_ALGO_LITERAL)
+            return nnqs_set_error(NNQS_E_ARG, "nnqs_options.algorithm must be 0 or 1");
+        if (opt->thr_single < 0 || opt->thr_double < 0 || opt->thr_rowheavy < 0)
+            return nnqs_set_error(NNQS_E_ARG, "nnqs_options thresholds must be >= 0");
+        o.algorithm = opt->algorithm;
+        if (opt->thr_single) o.thr_single = opt->thr_single;
+        if (opt->thr_double) o.thr_double = opt->thr_double;
+        if (opt->thr_rowheavy) o.thr_rowheavy = opt->thr_rowheavy;
+    }
+    if (o.thr_rowheavy < o.thr_single) o.thr_rowheavy = o.thr_single;   // join rows must be in the multimap
     if (mode == 0 && n > 0 && !keys) return nnqs_set_error(NNQS_E_ARG, "sample-aware mode needs keys");
     if (mode == 0 && n >= (int64_t)0xFFFFFFFFLL) return nnqs_set_error(NNQS_E_SIZE, "table larger than 2^32-1 keys");
     if (mode == 1) {
@@ -213,17 +259,29 @@ int nnqs_table_prepare(nnqs_ham h, int mode, const uint64_t *keys, const double 
     t->n = n;
     t->device = h->device;
     t->stream = cuda_stream;
+    t->opt = o;
     DeviceGuard g(h->device);
     if (!g.ok) {
         delete t;
         return nnqs_set_error(NNQS_E_CUDA, "cudaSetDevice failed");
     }
-    configure_pool(h->device);
-    int rc = nnqs_table_build(t, keys, logpsi, cuda_stream);
+    int rc = NNQS_OK;
+    for (int i = 0; i < 3 && !rc; ++i) {
+        cudaStream_t s = nullptr;
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess)
+            rc = nnqs_set_error(NNQS_E_CUDA, "cudaStreamCreate failed");
+        t->own[i] = s;
+    }
+    cudaEvent_t ev = nullptr;
+    if (!rc && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+        rc = nnqs_set_error(NNQS_E_CUDA, "cudaEventCreate failed");
+    t->last_use = ev;
+    if (!rc) rc = nnqs_table_build(t, keys, logpsi, cuda_stream);
     if (!rc && mode == 0) rc = nnqs_table_build_spin(h, t, cuda_stream);
+    if (!rc) cudaEventRecord((cudaEvent_t)t->last_use, (cudaStream_t)cuda_stream);
     if (rc) {
-        nnqs_table_release(t);
-        delete t;
+        cudaStreamSynchronize((cudaStream_t)cuda_stream);
+        nnqs_table_free(t);
         return rc;
     }
     *out = t;
@@ -234,10 +292,26 @@ int nnqs_table_free(nnqs_table t) {
     if (!t) return NNQS_OK;
     {
         DeviceGuard g(t->device);
+        // release on the table's own stream, ordered after the last call that used it
+        cudaStream_t rs = (cudaStream_t)t->own[0];
+        if (rs && t->last_use) cudaStreamWaitEvent(rs, (cudaEvent_t)t->last_use, 0);
+        t->stream = rs;
         nnqs_table_release_spin(t);
         nnqs_table_release(t);
+        for (void *&s : t->own)
+            if (s) { cudaStreamDestroy((cudaStream_t)s); s = nullptr; }   // pending frees still complete
+        if (t->last_use) cudaEventDestroy((cudaEvent_t)t->last_use);
+        t->last_use = nullptr;
     }
     delete t;
+    return NNQS_OK;
+}
+
+int nnqs_table_set_algorithm(nnqs_table t, int algorithm) {
+    if (!t) return nnqs_set_error(NNQS_E_ARG, "nnqs_table_set_algorithm: null table");
+    if (algorithm != NNQS_ALGO_AUTO && algorithm != NNQS_ALGO_LITERAL)
+        return nnqs_set_error(NNQS_E_ARG, "algorithm must be 0 or 1");
+    t->opt.algorithm = algorithm;
     return NNQS_OK;
 }
 
@@ -247,9 +321,11 @@ int nnqs_table_info(nnqs_table t, int64_t *n, double *shift, int64_t *device_byt
     if (device_bytes) *device_bytes = t->bytes;
     if (shift) {
         DeviceGuard g(t->device);
+        cudaStream_t rs = (cudaStream_t)t->own[0];
         u64 k = 0;
-        cudaError_t e = cudaMemcpyAsync(&k, t->shift_key, 8, cudaMemcpyDeviceToHost, (cudaStream_t)t->stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)t->stream);
+        cudaError_t e = cudaStreamWaitEvent(rs, (cudaEvent_t)t->last_use, 0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&k, t->shift_key, 8, cudaMemcpyDeviceToHost, rs);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(rs);
         if (e != cudaSuccess) return nnqs_set_error(NNQS_E_CUDA, cudaGetErrorString(e));
         if (k == 0) *shift = 0.0;
         else {
@@ -260,10 +336,44 @@ int nnqs_table_info(nnqs_table t, int64_t *n, double *shift, int64_t *device_byt
     return NNQS_OK;
 }
 
-int nnqs_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_t *rows,
-                      const double *row_logpsi, int64_t n_rows, double *eloc_out, int64_t *stats_out,
-                      void *cuda_stream) {
-    if (!h || !t || n_rows < 0 || (n_rows > 0 && !eloc_out))
+namespace {
+bool structured_rows(nnqs_ham h, nnqs_table t, const uint64_t *rows) {
+    return !rows && t->spin_ready && h->spin.ok && t->opt.algorithm != NNQS_ALGO_LITERAL;
+}
+
+// One local-energy launch sequence (both algorithms), the fused Eq. (6) chunk
+// partials and the hit log included; records the table's last-use event.
+int local_energy_impl(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_t *rows, const double *row_logpsi,
+                      int64_t n_rows, double *eloc_out, const int64_t *counts, double *partials_out,
+                      int64_t *stats_out, const HitLogHost &lg, void *cuda_stream) {
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    ChunkSink cs;
+    unsigned *ctr = nullptr;
+    int rc = NNQS_OK;
+    if (partials_out && n_rows > 0) {
+        const int64_t nch = (n_rows + NNQS_REDUCE_CHUNK - 1) / NNQS_REDUCE_CHUNK;
+        cudaError_t e = nnqs_malloc_async((void **)&ctr, 4 * (size_t)nch, st);
+        if (e != cudaSuccess) return nnqs_set_error(NNQS_E_NOMEM, cudaGetErrorString(e));
+        cudaMemsetAsync(ctr, 0, 4 * (size_t)nch, st);
+        cs.counts = counts;
+        cs.partials = partials_out;
+        cs.ctr = ctr;
+    }
+    if (n_rows > 0) {
+        if (structured_rows(h, t, rows))
+            rc = nnqs_launch_local_energy_spin(h, t, row_begin, n_rows, eloc_out, stats_out, cs, lg, cuda_stream);
+        else
+            rc = nnqs_launch_local_energy(h, t, row_begin, rows, row_logpsi, n_rows, eloc_out, stats_out, cs,
+                                          cuda_stream);
+    }
+    if (ctr) cudaFreeAsync(ctr, st);
+    cudaEventRecord((cudaEvent_t)t->last_use, st);
+    return rc;
+}
+
+int local_energy_args(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_t *rows, const double *row_logpsi,
+                      int64_t n_rows, double *eloc_out, const int64_t *counts, double *partials_out) {
+    if (!h || !t || n_rows < 0 || (n_rows > 0 && !eloc_out) || (!counts != !partials_out))
         return nnqs_set_error(NNQS_E_ARG, "nnqs_local_energy: bad arguments");
     if (t->device != h->device) return nnqs_set_error(NNQS_E_ARG, "table and Hamiltonian on different devices");
     if (rows) {
@@ -271,20 +381,30 @@ int nnqs_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_
     } else if (row_begin < 0 || row_begin + n_rows > t->n) {
         return nnqs_set_error(NNQS_E_TABLE, "row range outside the table");
     }
+    return NNQS_OK;
+}
+}  // namespace
+
+int nnqs_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_t *rows,
+                      const double *row_logpsi, int64_t n_rows, double *eloc_out, const int64_t *counts,
+                      double *partials_out, int64_t *stats_out, void *cuda_stream) {
+    int rc = local_energy_args(h, t, row_begin, rows, row_logpsi, n_rows, eloc_out, counts, partials_out);
+    if (rc) return rc;
     DeviceGuard g(h->device);
     if (!g.ok) return nnqs_set_error(NNQS_E_CUDA, "cudaSetDevice failed");
-    if (!rows && t->spin_ready && h->spin.ok && g_algorithm != 1) {
-        if (n_rows == 0) return NNQS_OK;
-        return nnqs_launch_local_energy_spin(h, t, row_begin, n_rows, eloc_out, stats_out, cuda_stream);
-    }
-    return nnqs_launch_local_energy(h, t, row_begin, rows, row_logpsi, n_rows, eloc_out, stats_out, cuda_stream);
+    return local_energy_impl(h, t, row_begin, rows, row_logpsi, n_rows, eloc_out, counts, partials_out, stats_out,
+                             HitLogHost{}, cuda_stream);
 }
 
 int nnqs_chunk_work(nnqs_table t, int64_t chunk, int64_t *work_out, int64_t *floor_out, void *cuda_stream) {
     if (!t || chunk <= 0 || (t->n > 0 && !work_out)) return nnqs_set_error(NNQS_E_ARG, "nnqs_chunk_work: bad arguments");
     DeviceGuard g(t->device);
     if (!g.ok) return nnqs_set_error(NNQS_E_CUDA, "cudaSetDevice failed");
-    if (t->spin_ready && g_algorithm != 1) return nnqs_chunk_work_spin(t, chunk, work_out, floor_out, cuda_stream);
+    if (t->spin_ready && t->opt.algorithm != NNQS_ALGO_LITERAL) {
+        const int rc = nnqs_chunk_work_spin(t, chunk, work_out, floor_out, cuda_stream);
+        cudaEventRecord((cudaEvent_t)t->last_use, (cudaStream_t)cuda_stream);
+        return rc;
+    }
     const int64_t nch = (t->n + chunk - 1) / chunk;   // literal loop: every row costs K' pair tests
     for (int64_t c = 0; c < nch; ++c) {
         work_out[c] = std::min(chunk, t->n - c * chunk);
@@ -293,13 +413,82 @@ int nnqs_chunk_work(nnqs_table t, int64_t chunk, int64_t *work_out, int64_t *flo
     return NNQS_OK;
 }
 
-int nnqs_set_algorithm(int algorithm) {
-    if (algorithm != 0 && algorithm != 1) return nnqs_set_error(NNQS_E_ARG, "algorithm must be 0 or 1");
-    g_algorithm = algorithm;
-    return NNQS_OK;
+int nnqs_coupled_debug_rows(nnqs_ham h, nnqs_table t, int64_t row_begin, int64_t n_rows, int64_t max_pairs,
+                            int64_t *row_id, int64_t *group_id, uint64_t *xprime, int64_t *table_idx,
+                            double *h_xxp, int64_t *n_pairs_out) {
+    if (!n_pairs_out || max_pairs < 0) return nnqs_set_error(NNQS_E_ARG, "nnqs_coupled_debug_rows: bad arguments");
+    int rc = local_energy_args(h, t, row_begin, nullptr, nullptr, n_rows, (double *)1, nullptr, nullptr);
+    if (rc) return rc;
+    DeviceGuard g(h->device);
+    if (!g.ok) return nnqs_set_error(NNQS_E_CUDA, "cudaSetDevice failed");
+    cudaStream_t st = (cudaStream_t)t->own[0];
+    cudaStreamWaitEvent(st, (cudaEvent_t)t->last_use, 0);
+    const size_t cap = (size_t)(max_pairs > 0 ? max_pairs : 1);
+    const size_t bytes = 16 * (size_t)(n_rows + 1) + cap * 24 + 64;
+    char *buf = nullptr;
+    cudaError_t e = cudaMalloc((void **)&buf, bytes);
+    if (e != cudaSuccess) return nnqs_set_error(NNQS_E_NOMEM, cudaGetErrorString(e));
+    double *eloc = (double *)buf;
+    HitLogHost lg;
+    lg.count = (unsigned long long *)(buf + 16 * (size_t)(n_rows + 1));
+    lg.cap = (long long)cap;
+    lg.row = (long long *)((char *)lg.count + 64);
+    lg.idx = lg.row + cap;
+    lg.h = (double *)(lg.idx + cap);
+    cudaMemsetAsync(lg.count, 0, 8, st);
+    rc = local_energy_impl(h, t, row_begin, nullptr, nullptr, n_rows, eloc, nullptr, nullptr, nullptr, lg, st);
+    unsigned long long cnt = 0;
+    if (!rc) rc = cudaMemcpyAsync(&cnt, lg.count, 8, cudaMemcpyDeviceToHost, st) == cudaSuccess ? NNQS_OK
+                  : nnqs_set_error(NNQS_E_CUDA, "read hit count");
+    if (!rc && cudaStreamSynchronize(st) != cudaSuccess) rc = nnqs_set_error(NNQS_E_CUDA, "sync");
+    if (!rc) {
+        const size_t m = std::min<size_t>((size_t)cnt, cap);
+        std::vector<long long> hr(m), hi(m);
+        std::vector<double> hh(m);
+        if (m) {
+            cudaMemcpy(hr.data(), lg.row, 8 * m, cudaMemcpyDeviceToHost);
+            cudaMemcpy(hi.data(), lg.idx, 8 * m, cudaMemcpyDeviceToHost);
+            cudaMemcpy(hh.data(), lg.h, 8 * m, cudaMemcpyDeviceToHost);
+        }
+        // keys of the rows and of x' (mode 0: the table's keys; mode 1: the index)
+        std::vector<u64> keys;
+        if (t->mode == 0 && t->n > 0) {
+            keys.resize(2 * (size_t)t->n);
+            cudaMemcpy(keys.data(), t->keys, 16 * (size_t)t->n, cudaMemcpyDeviceToHost);
+        }
+        const HostTable &H = h->host;
+        const int64_t K = (int64_t)H.off.size() - 1;
+        auto key_of = [&](long long i, u64 &lo, u64 &hi2) {
+            if (t->mode == 0) { lo = keys[2 * i]; hi2 = keys[2 * i + 1]; }
+            else { lo = (u64)i; hi2 = 0; }
+        };
+        for (size_t j = 0; j < m && j < (size_t)max_pairs; ++j) {
+            u64 x0, x1, y0, y1;
+            key_of(hr[j], x0, x1);
+            key_of(hi[j], y0, y1);
+            if (row_id) row_id[j] = hr[j];
+            if (table_idx) table_idx[j] = hi[j];
+            if (h_xxp) h_xxp[j] = hh[j];
+            if (xprime) { xprime[2 * j] = y0; xprime[2 * j + 1] = y1; }
+            if (group_id) {   // groups ascending by 128-bit X (word1, then word0)
+                const u64 X0 = x0 ^ y0, X1 = x1 ^ y1;
+                int64_t lo = 0, hi3 = K - 1, found = -1;
+                while (lo <= hi3) {
+                    const int64_t mid = (lo + hi3) / 2;
+                    const u64 m0 = H.x[2 * mid], m1 = H.x[2 * mid + 1];
+                    if (m1 == X1 && m0 == X0) { found = mid; break; }
+                    if (m1 < X1 || (m1 == X1 && m0 < X0)) lo = mid + 1; else hi3 = mid - 1;
+                }
+                group_id[j] = found;
+            }
+        }
+        *n_pairs_out = (int64_t)cnt;
+        if ((int64_t)cnt > max_pairs) rc = nnqs_set_error(NNQS_E_SIZE, "max_pairs too small");
+    }
+    cudaStreamSynchronize(st);
+    cudaFree(buf);
+    return rc;
 }
-
-int nnqs_get_algorithm(void) { return g_algorithm; }
 
 int nnqs_coupled_debug(nnqs_ham h, nnqs_table t, const uint64_t *rows_host, int64_t n_rows,
                        int64_t max_pairs, int64_t *row_id, int64_t *group_id, uint64_t *xprime,
@@ -307,7 +496,8 @@ int nnqs_coupled_debug(nnqs_ham h, nnqs_table t, const uint64_t *rows_host, int6
     if (!h || !t || !rows_host || n_rows < 0 || max_pairs < 0 || !n_pairs_out)
         return nnqs_set_error(NNQS_E_ARG, "nnqs_coupled_debug: bad arguments");
     DeviceGuard g(h->device);
-    cudaStream_t st = (cudaStream_t)t->stream;
+    cudaStream_t st = (cudaStream_t)t->own[0];
+    cudaStreamWaitEvent(st, (cudaEvent_t)t->last_use, 0);
     void *buf = nullptr;
     const size_t cap = (size_t)(max_pairs > 0 ? max_pairs : 1);
     const size_t bytes = 16 * (size_t)n_rows + cap * (24 + 16 + 8) + 16;

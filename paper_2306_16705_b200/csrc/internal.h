@@ -5,6 +5,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "../../include/nnqs.h"
 
 typedef unsigned long long u64;
@@ -113,7 +115,10 @@ struct nnqs_table_s {
     int mode = 0;             // 0 sample-aware, 1 exact
     int device = 0;
     int64_t n = 0;
-    void *stream = nullptr;
+    void *stream = nullptr;   // the prepare stream (build only)
+    nnqs_options opt{};       // per-table options (include/nnqs.h)
+    void *own[3] = {nullptr, nullptr, nullptr};   // private streams: release, join, phase (ii)
+    void *last_use = nullptr; // cudaEvent_t recorded after every call using the table
     void *keys = nullptr;     // ulonglong2 [n] (mode 0)
     void *logpsi = nullptr;   // double2 [n]
     void *psi_hat = nullptr;  // double2 [n]
@@ -158,10 +163,24 @@ struct nnqs_table_s {
 
 int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream);
 void nnqs_table_release_spin(nnqs_table t);
+// fused first pass of Eq. (6) per chunk of NNQS_REDUCE_CHUNK rows (nnqs_local_energy's
+// counts / partials_out): ctr = device u32[n_chunks] zeroed by the caller
+struct ChunkSink {
+    const int64_t *counts = nullptr;
+    double *partials = nullptr;
+    unsigned *ctr = nullptr;
+};
+// parity hit log of the production path (nnqs_coupled_debug_rows); count == nullptr: off
+struct HitLogHost {
+    unsigned long long *count = nullptr;
+    long long cap = 0;
+    long long *row = nullptr, *idx = nullptr;
+    double *h = nullptr;
+};
 int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, int64_t n_rows,
-                                  double *eloc, int64_t *stats, void *stream);
+                                  double *eloc, int64_t *stats, const ChunkSink &cs, const HitLogHost &lg,
+                                  void *stream);
 int nnqs_chunk_work_spin(nnqs_table t, int64_t chunk, int64_t *work_host, int64_t *floor_host, void *stream);
-int nnqs_algorithm();
 
 // device side (kernels.cu)
 int nnqs_ham_upload(nnqs_ham h);
@@ -170,7 +189,13 @@ int nnqs_table_build(nnqs_table t, const uint64_t *keys, const double *logpsi, v
 void nnqs_table_release(nnqs_table t);
 int nnqs_launch_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_t *rows,
                              const double *row_logpsi, int64_t n_rows, double *eloc,
-                             int64_t *stats, void *stream);
+                             int64_t *stats, const ChunkSink &cs, void *stream);
+// stream-ordered allocation from the library's own memory pool (one per device,
+// created once, thread-safe; the device's default pool is left untouched)
+cudaError_t nnqs_malloc_async(void **p, size_t bytes, cudaStream_t st);
+template <class T> inline cudaError_t nnqs_malloc_async(T **p, size_t bytes, cudaStream_t st) {
+    return nnqs_malloc_async(reinterpret_cast<void **>(p), bytes, st);
+}
 int nnqs_launch_coupled_debug(nnqs_ham h, nnqs_table t, const uint64_t *rows_dev, int64_t n_rows,
                               int64_t max_pairs, int64_t *out_i64 /*[max][3]*/, u64 *out_x /*[max][2]*/,
                               double *out_h, unsigned long long *counter, void *stream);

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 
+#include "common.cuh"
 #include "internal.h"
 
 #define NNQS_EMPTY_SLOT 0xFFFFFFFFFFFFFFFFULL
@@ -193,7 +194,7 @@ template <int MODE, bool CONS>
 __global__ void __launch_bounds__(256) k_eloc_v1(HamView H, TabView T, int64_t row_begin,
                                                  const ulonglong2 *rows, const double2 *row_lp,
                                                  int64_t n_rows, double2 *out,
-                                                 unsigned long long *stats) {
+                                                 unsigned long long *stats, ChunkSink cs) {
     const double s = dkey_inv(*T.shift_key);
     u64 c_pairs = 0, c_sec = 0, c_hit = 0, c_str = 0;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows;
@@ -216,6 +217,7 @@ __global__ void __launch_bounds__(256) k_eloc_v1(HamView H, TabView T, int64_t r
         }
         if (!(lx.x > -INFINITY)) {                 // psi(x) = 0: 0/0 (reading R10)
             out[r] = make_double2(NAN, NAN);
+            chunk_done_thread(cs, out, r, n_rows);
             continue;
         }
         const double rel = lx.x - s;
@@ -264,6 +266,7 @@ __global__ void __launch_bounds__(256) k_eloc_v1(HamView H, TabView T, int64_t r
             e = make_double2(ar * ir - ai * ii, ar * ii + ai * ir);
         }
         out[r] = e;
+        chunk_done_thread(cs, out, r, n_rows);   // fused first pass of Eq. (6)
     }
     if (stats) {
         for (int o = 16; o; o >>= 1) {
@@ -318,44 +321,20 @@ __global__ void k_coupled_debug(HamView H, TabView T, const ulonglong2 *rows, in
 }
 
 // ------------------------------------------------------------ energy reduce
-// one 256-thread block per chunk of NNQS_REDUCE_CHUNK rows; fixed tree order
+// one warp per chunk of NNQS_REDUCE_CHUNK rows, 8 chunks per block; the fixed
+// order of chunk_partial_warp (common.cuh), shared with the fused epilogues
 __global__ void __launch_bounds__(256) k_chunk_partials(const double2 *eloc, const int64_t *counts,
                                                         int64_t n, const double *mean,
                                                         double *partials) {
-    __shared__ double sa[256], sb[256], sc[256];
-    const int64_t base = (int64_t)blockIdx.x * NNQS_REDUCE_CHUNK;
-    double a = 0.0, b = 0.0, c = 0.0;
-    double mr = 0.0, mi = 0.0;
-    if (mean) { mr = mean[0]; mi = mean[1]; }
-    for (int j = 0; j < NNQS_REDUCE_CHUNK / 256; ++j) {
-        const int64_t i = base + threadIdx.x + 256 * j;
-        if (i < n) {
-            const double w = (double)counts[i];
-            const double2 e = eloc[i];
-            a += w;
-            if (!mean) {
-                b = fma(w, e.x, b);
-                c = fma(w, e.y, c);
-            } else {
-                const double dr = e.x - mr, di = e.y - mi;
-                b = fma(w, dr * dr + di * di, b);
-            }
-        }
-    }
-    sa[threadIdx.x] = a; sb[threadIdx.x] = b; sc[threadIdx.x] = c;
-    __syncthreads();
-    for (int s = 128; s; s >>= 1) {
-        if (threadIdx.x < s) {
-            sa[threadIdx.x] += sa[threadIdx.x + s];
-            sb[threadIdx.x] += sb[threadIdx.x + s];
-            sc[threadIdx.x] += sc[threadIdx.x + s];
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        partials[3 * blockIdx.x] = sa[0];
-        partials[3 * blockIdx.x + 1] = sb[0];
-        partials[3 * blockIdx.x + 2] = sc[0];
+    const int64_t ch = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int64_t base = ch * NNQS_REDUCE_CHUNK;
+    if (base >= n) return;
+    const int len = (int)min((int64_t)NNQS_REDUCE_CHUNK, n - base);
+    const double3 p = chunk_partial_warp<false>(eloc, counts, base, len, mean);
+    if ((threadIdx.x & 31) == 0) {
+        partials[3 * ch] = p.x;
+        partials[3 * ch + 1] = p.y;
+        partials[3 * ch + 2] = mean ? 0.0 : p.z;
     }
 }
 
@@ -446,11 +425,11 @@ int nnqs_table_build(nnqs_table t, const uint64_t *keys, const double *logpsi, v
     const int64_t n = t->n;
     size_t bk = 16 * (size_t)n;
     // shift key + flag in one small allocation
-    if ((rc = cuda_check(cudaMallocAsync((void **)&t->shift_key, 16, st), "alloc shift"))) return rc;
+    if ((rc = cuda_check(nnqs_malloc_async((void **)&t->shift_key, 16, st), "alloc shift"))) return rc;
     t->flag = (int *)(t->shift_key + 1);
     if ((rc = cuda_check(cudaMemsetAsync(t->shift_key, 0, 16, st), "memset shift"))) return rc;
-    if ((rc = cuda_check(cudaMallocAsync(&t->logpsi, bk ? bk : 16, st), "alloc logpsi"))) return rc;
-    if ((rc = cuda_check(cudaMallocAsync(&t->psi_hat, bk ? bk : 16, st), "alloc psi_hat"))) return rc;
+    if ((rc = cuda_check(nnqs_malloc_async(&t->logpsi, bk ? bk : 16, st), "alloc logpsi"))) return rc;
+    if ((rc = cuda_check(nnqs_malloc_async(&t->psi_hat, bk ? bk : 16, st), "alloc psi_hat"))) return rc;
     if (n) {
         if ((rc = cuda_check(cudaMemcpyAsync(t->logpsi, logpsi, bk, cudaMemcpyDeviceToDevice, st), "copy logpsi"))) return rc;
     }
@@ -459,8 +438,8 @@ int nnqs_table_build(nnqs_table t, const uint64_t *keys, const double *logpsi, v
         u64 nb = 1;
         while (nb * 4 < 2 * (u64)(n > 0 ? n : 1)) nb <<= 1;   // load factor <= 1/2
         t->bucket_mask = nb - 1;
-        if ((rc = cuda_check(cudaMallocAsync(&t->keys, bk ? bk : 16, st), "alloc keys"))) return rc;
-        if ((rc = cuda_check(cudaMallocAsync((void **)&t->slots, 32 * nb, st), "alloc slots"))) return rc;
+        if ((rc = cuda_check(nnqs_malloc_async(&t->keys, bk ? bk : 16, st), "alloc keys"))) return rc;
+        if ((rc = cuda_check(nnqs_malloc_async((void **)&t->slots, 32 * nb, st), "alloc slots"))) return rc;
         if (n) {
             if ((rc = cuda_check(cudaMemcpyAsync(t->keys, keys, bk, cudaMemcpyDeviceToDevice, st), "copy keys"))) return rc;
         }
@@ -498,7 +477,7 @@ void nnqs_table_release(nnqs_table t) {
 
 int nnqs_launch_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_t *rows,
                              const double *row_logpsi, int64_t n_rows, double *eloc,
-                             int64_t *stats, void *stream) {
+                             int64_t *stats, const ChunkSink &cs, void *stream) {
     if (n_rows == 0) return NNQS_OK;
     cudaStream_t st = (cudaStream_t)stream;
     HamView H = ham_view(h);
@@ -510,11 +489,11 @@ int nnqs_launch_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const 
     auto *o = (double2 *)eloc;
     auto *s = (unsigned long long *)stats;
     if (t->mode == 0) {
-        if (cons) k_eloc_v1<0, true><<<g, 256, 0, st>>>(H, T, row_begin, r, rl, n_rows, o, s);
-        else k_eloc_v1<0, false><<<g, 256, 0, st>>>(H, T, row_begin, r, rl, n_rows, o, s);
+        if (cons) k_eloc_v1<0, true><<<g, 256, 0, st>>>(H, T, row_begin, r, rl, n_rows, o, s, cs);
+        else k_eloc_v1<0, false><<<g, 256, 0, st>>>(H, T, row_begin, r, rl, n_rows, o, s, cs);
     } else {
-        if (cons) k_eloc_v1<1, true><<<g, 256, 0, st>>>(H, T, row_begin, r, rl, n_rows, o, s);
-        else k_eloc_v1<1, false><<<g, 256, 0, st>>>(H, T, row_begin, r, rl, n_rows, o, s);
+        if (cons) k_eloc_v1<1, true><<<g, 256, 0, st>>>(H, T, row_begin, r, rl, n_rows, o, s, cs);
+        else k_eloc_v1<1, false><<<g, 256, 0, st>>>(H, T, row_begin, r, rl, n_rows, o, s, cs);
     }
     return cuda_check(cudaGetLastError(), "local energy launch");
 }
@@ -546,7 +525,7 @@ extern "C" int nnqs_energy_chunk_partials(const double *eloc, const int64_t *cou
         return nnqs_set_error(NNQS_E_ARG, "nnqs_energy_chunk_partials: bad arguments");
     if (n == 0) return NNQS_OK;
     const int64_t chunks = (n + NNQS_REDUCE_CHUNK - 1) / NNQS_REDUCE_CHUNK;
-    k_chunk_partials<<<(unsigned)chunks, 256, 0, (cudaStream_t)cuda_stream>>>(
+    k_chunk_partials<<<(unsigned)((chunks + 7) / 8), 256, 0, (cudaStream_t)cuda_stream>>>(
         (const double2 *)eloc, counts, n, mean_dev, partials);
     return cuda_check(cudaGetLastError(), "chunk partials launch");
 }
@@ -589,12 +568,12 @@ extern "C" int nnqs_energy_reduce(const double *eloc, const int64_t *counts, int
     cudaStream_t st = (cudaStream_t)cuda_stream;
     const int64_t chunks = (n + NNQS_REDUCE_CHUNK - 1) / NNQS_REDUCE_CHUNK;
     double *buf = nullptr;
-    int rc = cuda_check(cudaMallocAsync((void **)&buf, sizeof(double) * (3 * chunks + 8), st), "alloc reduce");
+    int rc = cuda_check(nnqs_malloc_async((void **)&buf, sizeof(double) * (3 * chunks + 8), st), "alloc reduce");
     if (rc) return rc;
     double *part = buf, *o1 = buf + 3 * chunks, *o2 = o1 + 4;
-    k_chunk_partials<<<(unsigned)chunks, 256, 0, st>>>((const double2 *)eloc, counts, n, nullptr, part);
+    k_chunk_partials<<<(unsigned)((chunks + 7) / 8), 256, 0, st>>>((const double2 *)eloc, counts, n, nullptr, part);
     k_combine<<<1, 32, 0, st>>>(part, chunks, 1, o1);
-    k_chunk_partials<<<(unsigned)chunks, 256, 0, st>>>((const double2 *)eloc, counts, n, o1, part);
+    k_chunk_partials<<<(unsigned)((chunks + 7) / 8), 256, 0, st>>>((const double2 *)eloc, counts, n, o1, part);
     k_combine<<<1, 32, 0, st>>>(part, chunks, 2, o2);
     double h[8];
     rc = cuda_check(cudaMemcpyAsync(h, o1, sizeof(h), cudaMemcpyDeviceToHost, st), "read reduce");
@@ -610,7 +589,7 @@ extern "C" int nnqs_local_energy_check(const double *eloc, int64_t n, void *cuda
     if (n < 0 || (n > 0 && !eloc)) return nnqs_set_error(NNQS_E_ARG, "nnqs_local_energy_check: bad arguments");
     cudaStream_t st = (cudaStream_t)cuda_stream;
     int *flag = nullptr;
-    int rc = cuda_check(cudaMallocAsync((void **)&flag, sizeof(int), st), "alloc flag");
+    int rc = cuda_check(nnqs_malloc_async((void **)&flag, sizeof(int), st), "alloc flag");
     if (rc) return rc;
     cudaMemsetAsync(flag, 0, sizeof(int), st);
     if (n) k_any_nan<<<grid_for(2 * n, 256), 256, 0, st>>>(eloc, 2 * n, flag);

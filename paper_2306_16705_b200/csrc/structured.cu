@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "common.cuh"
 #include "internal.h"
 
 __constant__ u64 c_hs[128];   // same GF(2) hash columns as kernels.cu (per translation unit)
@@ -101,6 +102,24 @@ __device__ __forceinline__ double g_d(const GroupView &G, uint32_t i) {
     return __longlong_as_double((long long)__ldg(G.rec + 2 * i + 1).x);
 }
 
+// Parity/debug hit log (nnqs_coupled_debug_rows): every hit the production
+// kernels evaluate is appended as (row, x' table index, H_xx').  count == nullptr
+// (the normal call) disables it: one warp-uniform branch per evaluated batch.
+struct HitLog {
+    unsigned long long *count;
+    long long cap;
+    long long *row, *idx;
+    double *h;
+};
+__device__ __forceinline__ void log_hit(const HitLog &L, int row, long long idx, double hv) {
+    const unsigned long long s = atomicAdd(L.count, 1ULL);
+    if ((long long)s < L.cap) {
+        L.row[s] = row;
+        L.idx[s] = idx;
+        L.h[s] = hv;
+    }
+}
+
 struct TabSpin {
     int64_t n;
     const ulonglong2 *keys;
@@ -126,6 +145,7 @@ struct TabSpin {
     int32_t thr_single, thr_double;
     int uniform_pc;           // every alpha (beta) string of the table has one popcount: XOR
                               // distance 2 / 4 already implies a balanced excitation
+    HitLog log;               // parity hit log (count == nullptr: off)
 };
 
 // ---------------------------------------------------------------- multimap
@@ -306,7 +326,7 @@ struct RowState {
     u64 x0, x1;
     double2 lx;
     int direct;
-    int pad;
+    int row;        // table index of the row (hit log)
 };
 
 // Inlined at every push site: the ratio psi(x')/psi(x) of the rare rows with
@@ -316,7 +336,7 @@ struct RowState {
 template <bool DIRECT, bool OCC>
 __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *psi_hat, const double2 *logpsi,
                                              const int2 *q, int qh, int cnt, const RowState *rs, double2 *acc,
-                                             const double *occ_rec, int nq) {
+                                             const double *occ_rec, int nq, const HitLog &lg) {
     const int lane = threadIdx.x & 31;
     uint32_t c_hit = 0, c_str = 0;
     __syncwarp();
@@ -343,6 +363,7 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
         ++c_hit;
     }
     auto add = [&](double hv, int64_t idx) {
+        if (lg.count) log_hit(lg, rs->row, idx, hv);
         double2 ps = ps0;
         if (direct) {
             const double2 lx = rs->lx;
@@ -425,6 +446,13 @@ __device__ unsigned long long g_prof[16];
 #endif
 
 #define SCAN_LIMIT 8192
+// multimap sizing (measured): slots >= 4 x runs, 8 Bloom bits per run
+#define MM_LOAD 4.0
+#define MM_BLOOM_BITS 8
+// phases compiled into the launch sequence (profiling builds may mask some: -DNNQS_PHASE_MASK=...)
+#ifndef NNQS_PHASE_MASK
+#define NNQS_PHASE_MASK 15
+#endif
 #define WARPS_PER_BLOCK 8
 #ifndef NNQS_SPIN_MINB
 #define NNQS_SPIN_MINB 4
@@ -449,7 +477,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                                                    unsigned long long *stats, unsigned long long pairs,
                                                    int phase_mask, const double2 *acc_heavy, int32_t thr_rowheavy,
                                                    double2 *partial, unsigned long long *row_ctr,
-                                                   const int32_t *perm, double2 *partial2) {
+                                                   const int32_t *perm, double2 *partial2, ChunkSink cs) {
     __shared__ int2 s_q[WARPS_PER_BLOCK][QCAP];
     __shared__ uint8_t s_orb[WARPS_PER_BLOCK][4][64];   // occ(a), vir(a), occ(b), vir(b) of the row
     __shared__ int2 s_h[(PH & 8) ? WARPS_PER_BLOCK : 1][HCAP];   // heavy adjacent alpha groups (g, u rank)
@@ -499,6 +527,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
         const double2 lx0 = T.logpsi[i];
         if (!(lx0.x > -INFINITY)) {
             if (lane == 0 && (PH & 8) && !DIRECT) out[r] = make_double2(NAN, NAN);
+            if ((PH & 8) && !DIRECT) chunk_done_warp(cs, out, r, n_rows);
             continue;
         }
         if (((lx0.x - s) < -600.0) != DIRECT) continue;   // the other instantiation's row
@@ -510,6 +539,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             rs->x1 = xk.y;
             rs->lx = lx0;
             rs->direct = DIRECT;
+            rs->row = (int)i;
         }
         double2 a0 = make_double2(0.0, 0.0);         // 16: continue a row
         if ((PH & 16) && lane == 0) {
@@ -534,7 +564,8 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
         int qn = 0, qh = 0;                          // warp-uniform ring length and head
         auto flush = [&](int cnt) {                  // lanes < cnt evaluate q[qh + lane]
             PROF_T(t_fl)
-            const uint2 fo = flush_queue<DIRECT, (PH & 6) != 0>(G, T.psi_hat, T.logpsi, q, qh, cnt, rs, acc, S.occ_rec, S.nq);
+            const uint2 fo = flush_queue<DIRECT, (PH & 6) != 0>(G, T.psi_hat, T.logpsi, q, qh, cnt, rs, acc, S.occ_rec, S.nq,
+                                                                  T.log);
             c_hit += fo.x;
             c_str += fo.y;
             qh = (qh + cnt) & (QCAP - 1);
@@ -630,6 +661,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                 hv = warp_strided_sum(G, gb, ge, rs->x0, rs->x1);
             }
             if (lane == 0) {   // x' = x: psi_hat(x) (or 1 on the direct path)
+                if (T.log.count) log_hit(T.log, (int)i, i, hv);
                 double2 ps = make_double2(1.0, 0.0);
                 if (!DIRECT) ps = __ldg(T.psi_hat + i);
                 double2 ac = acc[0];
@@ -890,6 +922,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             }
             out[r] = e;
         }
+        if (PH & 8) chunk_done_warp(cs, out, r, n_rows);   // fused first pass of Eq. (6)
         PROF_ADD(7, t_row)
     }
     PROF_FLUSH
@@ -1374,6 +1407,7 @@ __global__ void k_hj_eval(SpinView S, GroupView G, TabSpin T, const int32_t *hea
                             hv += flip_sign2(g_d(G, i), (__popcll(xk.x & Z.x) + __popcll(xk.y & Z.y)) & 1);
                         }
                         c_str += b1[u] - b0[u];
+                        if (T.log.count) log_hit(T.log, e, ix[u], hv);
                         ar = fma(hv, ps[u].x, ar);
                         ai = fma(hv, ps[u].y, ai);
                         ++c_hit;
@@ -1393,6 +1427,7 @@ __global__ void k_hj_eval(SpinView S, GroupView G, TabSpin T, const int32_t *hea
                     k = S.ab_k[pair_rank(p1, p2, S.n) * S.P + pair_rank(r1, r2, S.n)];
                 }
                 const double hv = group_value1(G, k, xk.x, xk.y, c_str);
+                if (T.log.count) log_hit(T.log, e, idx, hv);
                 double2 ps;
                 if (!direct) {
                     ps = T.psi_hat[idx];
@@ -1894,12 +1929,12 @@ int ensure_binom(int device) {
 int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, void *, size_t) {
     const int g = grid_for(n, 256);
     int64_t *eoff = nullptr;
-    int rc = cuda_check(cudaMallocAsync((void **)&eoff, 8 * (n + 1), st), "alloc mm offsets");
+    int rc = cuda_check(nnqs_malloc_async((void **)&eoff, 8 * (n + 1), st), "alloc mm offsets");
     if (rc) return rc;
     // compact-key support: popcount range, dense ranks of the groups that receive keys
     const int64_t nga = t->n_alpha_groups;
     int32_t *rk = nullptr;                       // [pc_range 4 | flagA nga+1 | rankA | flagB n+1 | rankB]
-    rc = cuda_check(cudaMallocAsync((void **)&rk, 4 * (4 + 2 * (nga + 1) + 2 * (n + 1)) + 64, st), "alloc mm ranks");
+    rc = cuda_check(nnqs_malloc_async((void **)&rk, 4 * (4 + 2 * (nga + 1) + 2 * (n + 1)) + 64, st), "alloc mm ranks");
     if (rc) { cudaFreeAsync(eoff, st); return rc; }
     int *pcr = rk;
     int32_t *flagA = rk + 4, *rankA = flagA + nga + 1, *flagB = rankA + nga + 1, *rankB = flagB + n + 1;
@@ -1917,7 +1952,7 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
         cub::DeviceScan::ExclusiveSum(nullptr, ts1, flagA, rankA, (int)nga + 1, st);
         cub::DeviceScan::ExclusiveSum(nullptr, ts2, flagB, rankB, (int)n + 1, st);
         void *tsc = nullptr;
-        rc = cuda_check(cudaMallocAsync(&tsc, std::max(ts1, ts2), st), "alloc rank scan");
+        rc = cuda_check(nnqs_malloc_async(&tsc, std::max(ts1, ts2), st), "alloc rank scan");
         if (rc) { cudaFreeAsync(rk, st); cudaFreeAsync(eoff, st); return rc; }
         cub::DeviceScan::ExclusiveSum(tsc, ts1, flagA, rankA, (int)nga + 1, st);
         cub::DeviceScan::ExclusiveSum(tsc, ts2, flagB, rankB, (int)n + 1, st);
@@ -1927,11 +1962,11 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
     cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, eoff, (int)n + 1, st);
     void *stmp = nullptr;
     cudaMemsetAsync(eoff + n, 0, 8, st);
-    rc = cuda_check(cudaMallocAsync(&stmp, tb, st), "alloc scan tmp");
+    rc = cuda_check(nnqs_malloc_async(&stmp, tb, st), "alloc scan tmp");
     if (rc) { cudaFreeAsync(eoff, st); return rc; }
     // counts has n entries; scan n+1 with a zero appended (counts[n] read as 0)
     int32_t *cz = nullptr;
-    cudaMallocAsync((void **)&cz, 4 * (n + 1), st);
+    nnqs_malloc_async((void **)&cz, 4 * (n + 1), st);
     cudaMemcpyAsync(cz, counts, 4 * n, cudaMemcpyDeviceToDevice, st);
     cudaMemsetAsync(cz + n, 0, 4, st);
     cub::DeviceScan::ExclusiveSum(stmp, tb, cz, eoff, (int)n + 1, st);
@@ -1963,15 +1998,12 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
         kbits_all = rbits + mbits;
     }
     const bool compact = kbits_all <= 64 && ensure_binom(t->device) == NNQS_OK;
-    if (std::getenv("NNQS_VERBOSE"))
-        std::fprintf(stderr, "[nnqs] multimap: m=%lld kbits_all=%d rbits=%d NA=%d NB=%d pc=%d,%d,%d,%d\n", (long long)m,
-                     kbits_all, rbits, NA, NB, hpc[0], hpc[1], hpc[2], hpc[3]);
     t->uniform_pc = !rc && hpc[0] == hpc[1] && hpc[2] == hpc[3];
     if (rc || m == 0) {
         cudaFreeAsync(rk, st);
         cudaFreeAsync(eoff, st);
         if (!rc) {   // empty multimap: one empty slot
-            rc = cuda_check(cudaMallocAsync(&t->mm_buf, 128, st), "alloc mm");
+            rc = cuda_check(nnqs_malloc_async(&t->mm_buf, 128, st), "alloc mm");
             if (rc) return rc;
             t->mm = t->mm_buf;
             t->mm_mask = 0;
@@ -1999,7 +2031,7 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
     const size_t ctb = std::max(t1, std::max(t2, t3));
     const size_t sbytes = 4 * r16(8 * m) + 3 * r16(4 * m) + 4 * r16(4 * m) + r16(ctb) + 64;
     char *sc = nullptr;
-    rc = cuda_check(cudaMallocAsync((void **)&sc, sbytes, st), "alloc mm scratch");
+    rc = cuda_check(nnqs_malloc_async((void **)&sc, sbytes, st), "alloc mm scratch");
     if (rc) { cudaFreeAsync(rk, st); cudaFreeAsync(eoff, st); return rc; }
     char *sp = sc;
     auto take = [&](size_t b) { char *p = sp; sp += r16(b); return p; };
@@ -2035,23 +2067,12 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
     rc = cuda_check(cudaMemcpyAsync(&nruns, P1 + m - 1, 4, cudaMemcpyDeviceToHost, st), "read runs");
     if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
     if (rc) { cudaFreeAsync(sc, st); cudaFreeAsync(eoff, st); return rc; }
-    static double mm_load = -1.0;   // slots >= mm_load * runs (power of two); tuning: NNQS_MM_LOAD
-    if (mm_load < 0) {
-        const char *e = std::getenv("NNQS_MM_LOAD");
-        mm_load = e ? std::atof(e) : 4.0;   // measured: 2 -> 69.6, 3 -> 68.6, 5 -> 68.4, 9 -> 68.8 ms/step
-    }
-    u64 slots = 2;
-    while ((double)slots < mm_load * (double)nruns) slots <<= 1;
-    if (std::getenv("NNQS_VERBOSE")) std::fprintf(stderr, "[nnqs] multimap: runs=%d slots=%llu\n", nruns, slots);
-    static int bloom_bits = -1;   // Bloom bits per run (tuning: NNQS_BLOOM_BITS)
-    if (bloom_bits < 0) {
-        const char *e = std::getenv("NNQS_BLOOM_BITS");
-        bloom_bits = e ? std::max(1, std::atoi(e)) : 8;
-    }
+    u64 slots = 2;   // slots >= MM_LOAD * runs (power of two)
+    while ((double)slots < MM_LOAD * (double)nruns) slots <<= 1;
     u64 bwords = 1;
-    while (bwords * 64 < (u64)bloom_bits * (u64)nruns) bwords <<= 1;
+    while (bwords * 64 < (u64)MM_BLOOM_BITS * (u64)nruns) bwords <<= 1;
     const size_t pbytes = r16(32 * slots) + r16(16 * m) + r16(8 * bwords);
-    rc = cuda_check(cudaMallocAsync(&t->mm_buf, pbytes, st), "alloc multimap");
+    rc = cuda_check(nnqs_malloc_async(&t->mm_buf, pbytes, st), "alloc multimap");
     if (rc) { cudaFreeAsync(sc, st); cudaFreeAsync(eoff, st); return rc; }
     t->mm = t->mm_buf;
     t->mm_mask = slots - 1;
@@ -2093,10 +2114,10 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
     // scratch: iota, perm1, perm2 (int32), k1, k2 (u64), flags, incl (int32), cub temp
     const size_t scr = 5 * r16(4 * n) + 2 * r16(8 * n) + r16(tmp) + 16;
     char *buf = nullptr;
-    int rc = cuda_check(cudaMallocAsync((void **)&buf, pers, st), "alloc spin index");
+    int rc = cuda_check(nnqs_malloc_async((void **)&buf, pers, st), "alloc spin index");
     if (rc) return rc;
     char *scratch = nullptr;
-    rc = cuda_check(cudaMallocAsync((void **)&scratch, scr, st), "alloc spin scratch");
+    rc = cuda_check(nnqs_malloc_async((void **)&scratch, scr, st), "alloc spin scratch");
     if (rc) { cudaFreeAsync(buf, st); return rc; }
     t->spin_buf = buf;
     auto take = [&](size_t bytes) { char *p = buf; buf += (bytes + 15) & ~size_t(15); return p; };
@@ -2148,10 +2169,8 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
             k_csr<<<g, 256, 0, st>>>(k1, perm2, incl, n, t->sa, t->offB, t->gb_of, t->listB_a, t->listB_idx,
                                      nullptr, nullptr, 0);
     }
-    t->thr_single = 128;   // measured (step ms): 96 63.52, 128 63.45, 192 63.67, 256 64.15
-    t->thr_double = 8192;   // measured (step ms): 2048 69.46, 4096 63.51, 8192 63.15
-    if (const char *e = std::getenv("NNQS_THR_SINGLE")) t->thr_single = std::atoi(e);   // tuning only
-    if (const char *e = std::getenv("NNQS_THR_DOUBLE")) t->thr_double = std::atoi(e);
+    t->thr_single = t->opt.thr_single;   // per-table options (nnqs_options; defaults measured in DESIGN.md Sec. 7)
+    t->thr_double = t->opt.thr_double;
     // adjacent-alpha lists per alpha group (phase (iii) streams them instead of
     // repeating the 675 alpha-string lookups for every row of the group)
     {
@@ -2161,23 +2180,18 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
         const size_t rb = (8 * (size_t)ng + 15) & ~size_t(15);            // 16-B aligned regions
         const size_t cb = (4 * (size_t)ng + 15) & ~size_t(15);
         const size_t bytes = rb + 64 + cb + 16 * (size_t)(ng * maxc + 1);
-        rc = cuda_check(cudaMallocAsync(&t->nl_buf, bytes, st), "alloc nl");
+        rc = cuda_check(nnqs_malloc_async(&t->nl_buf, bytes, st), "alloc nl");
         if (rc) { cudaFreeAsync(scratch, st); return rc; }
         t->nl_rng = t->nl_buf;
         unsigned long long *cursor = (unsigned long long *)((char *)t->nl_buf + rb);
         t->nl_cost = (int32_t *)((char *)t->nl_buf + rb + 64);
         t->nl = (char *)t->nl_buf + rb + 64 + cb;
         t->bytes += (int64_t)bytes;
-        static int nl_join = -1;
-        if (nl_join < 0) {
-            const char *e = std::getenv("NNQS_NL_JOIN");
-            nl_join = e ? std::atoi(e) : 1;
-        }
-        if (nl_join && n_orb < 64) {
+        if (n_orb < 64) {
             // deletion join (see k_adel_*): ~n_alpha keys per group instead of
             // n_alpha x n_empty hash lookups
             int32_t *cnt = nullptr;
-            rc = cuda_check(cudaMallocAsync((void **)&cnt, 8 * (ng + 2), st), "alloc nl join counts");
+            rc = cuda_check(nnqs_malloc_async((void **)&cnt, 8 * (ng + 2), st), "alloc nl join counts");
             if (rc) { cudaFreeAsync(scratch, st); return rc; }
             int32_t *eoff = cnt + ng + 1;
             cudaMemsetAsync(cnt + ng, 0, 4, st);
@@ -2185,7 +2199,7 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
             size_t tb = 0;
             cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, eoff, (int)ng + 1, st);
             void *tmp0 = nullptr;
-            rc = cuda_check(cudaMallocAsync(&tmp0, tb, st), "alloc nl join scan");
+            rc = cuda_check(nnqs_malloc_async(&tmp0, tb, st), "alloc nl join scan");
             if (rc) { cudaFreeAsync(cnt, st); cudaFreeAsync(scratch, st); return rc; }
             cub::DeviceScan::ExclusiveSum(tmp0, tb, cnt, eoff, (int)ng + 1, st);
             cudaFreeAsync(tmp0, st);
@@ -2206,7 +2220,7 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
             auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
             char *w = nullptr;
             const size_t wb = 2 * al(8 * m) + 9 * al(4 * (m + 1)) + al(4 * (ng + 1)) + al(tt);
-            rc = cuda_check(cudaMallocAsync((void **)&w, wb, st), "alloc nl join work");
+            rc = cuda_check(nnqs_malloc_async((void **)&w, wb, st), "alloc nl join work");
             if (rc) { cudaFreeAsync(cnt, st); cudaFreeAsync(scratch, st); return rc; }
             char *wp = w;
             auto tk = [&](size_t x) { char *p0 = wp; wp += al(x); return p0; };
@@ -2251,8 +2265,7 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
     // deletion multimap for heavy groups (sorted CSR + unique-key hash)
     rc = build_multimap(t, n, st, flags, ctmp, tmp);
     if (rc) { cudaFreeAsync(scratch, st); return rc; }
-    t->thr_rowheavy = 16384;
-    if (const char *e = std::getenv("NNQS_THR_ROWHEAVY")) t->thr_rowheavy = std::atoi(e);   // tuning only
+    t->thr_rowheavy = t->opt.thr_rowheavy;
     if (t->thr_rowheavy < t->thr_single) t->thr_rowheavy = t->thr_single;   // rows must be in the multimap
     {
         int *cnt_d = (int *)incl;   // scratch reuse
@@ -2265,7 +2278,7 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
         if (rc) { cudaFreeAsync(scratch, st); return rc; }
         t->n_heavy = nh;
         if (nh) {
-            rc = cuda_check(cudaMallocAsync((void **)&t->heavy_groups, 4 * nh, st), "alloc heavy");
+            rc = cuda_check(nnqs_malloc_async((void **)&t->heavy_groups, 4 * nh, st), "alloc heavy");
             if (rc) { cudaFreeAsync(scratch, st); return rc; }
             // deterministic order of the heavy groups: sort the few ids on the host
             std::vector<int32_t> ids(nh);
@@ -2302,16 +2315,9 @@ int nnqs_chunk_work_spin(nnqs_table t, int64_t chunk, int64_t *work_host, int64_
     const int64_t nch = (t->n + chunk - 1) / chunk;
     if (nch == 0) return NNQS_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    static int w0 = -1, pd = -1, pj = -1, px = -1, pf = -1;   // estimate weights (knobs: NNQS_WORK_*)
-    if (w0 < 0) {
-        const char *a = std::getenv("NNQS_WORK_W0"), *b = std::getenv("NNQS_WORK_PD"), *c = std::getenv("NNQS_WORK_PJ");
-        const char *d = std::getenv("NNQS_WORK_PX"), *f = std::getenv("NNQS_WORK_PF");
-        pf = f ? std::atoi(f) : 32768;
-        w0 = a ? std::atoi(a) : 256;
-        pd = b ? std::atoi(b) : 4096;
-        pj = c ? std::atoi(c) : 4096;
-        px = d ? std::atoi(d) : 0;
-    }
+    // estimate weights: base per row, probed list, join row,
+    // probed x probed product, latency floor
+    const int w0 = 256, pd = 4096, pj = 4096, px = 0, pf = 32768;
     TabSpin tv{};
     tv.n = t->n;
     tv.ga_of = t->ga_of;
@@ -2319,7 +2325,7 @@ int nnqs_chunk_work_spin(nnqs_table t, int64_t chunk, int64_t *work_host, int64_
     tv.offA = t->offA;
     tv.offB = t->offB;
     long long *wd = nullptr;
-    int rc = cuda_check(cudaMallocAsync((void **)&wd, 16 * nch, st), "alloc chunk work");
+    int rc = cuda_check(nnqs_malloc_async((void **)&wd, 16 * nch, st), "alloc chunk work");
     if (rc) return rc;
     k_chunk_work<<<(unsigned)nch, 256, 0, st>>>(tv, chunk, t->thr_double, t->thr_rowheavy, t->nl_cost, w0, pd, pj, px,
                                                 pf, wd, wd + nch);
@@ -2332,7 +2338,7 @@ int nnqs_chunk_work_spin(nnqs_table t, int64_t chunk, int64_t *work_host, int64_
 }
 
 int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, int64_t n_rows, double *eloc,
-                                  int64_t *stats, void *stream) {
+                                  int64_t *stats, const ChunkSink &cs, const HitLogHost &lg, void *stream) {
     const SpinIndex &S = h->spin;
     const DeviceHam &D = h->dev;
     SpinView sv{S.n, S.P, D.pair_k[0], D.pair_k[1], D.quad_k[0], D.quad_k[1], D.ab_k, D.ab_rec ? D.ab_rec : D.ab_k,
@@ -2345,91 +2351,134 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
                t->listA_b, t->listB_a, t->listA_idx, t->listB_idx, t->ah_keys, t->ah_vals, t->ah_mask,
                (const ulonglong2 *)t->mm, t->mm_mask, t->mm_bloom, t->mm_bloom_mask,
                (const ulonglong2 *)t->mm_ent, (const int2 *)t->nl_rng, (const int4 *)t->nl, t->thr_single,
-               t->thr_double, t->uniform_pc ? 1 : 0};
-    const int64_t threads = n_rows * 32;
-    int g = (int)std::min<int64_t>((threads + 255) / 256, 148 * 64);
-    if (g < 1) g = 1;
+               t->thr_double, t->uniform_pc ? 1 : 0, HitLog{lg.count, lg.cap, lg.row, lg.idx, lg.h}};
     cudaStream_t st = (cudaStream_t)stream;
     int rc = ensure_hs(h->device);
     if (rc) return rc;
-    // stats[0] = row-group pairs resolved (the literal loop's R * K')
+    // stats[0] = row-group pairs resolved (the literal loop's R * K', by definition)
     const unsigned long long pairs = (unsigned long long)n_rows * (unsigned long long)h->n_groups;
-    static int phase_mask = -1;
-    if (phase_mask < 0) {
-        const char *e = std::getenv("NNQS_PHASE_MASK");   // debug / profiling only
-        phase_mask = e ? std::atoi(e) : 15;
-    }
-    double2 *acc_heavy = nullptr;
-    u64 *hkeys = nullptr;
-    void *htmp = nullptr;
-    unsigned long long *hcnt = nullptr;
+    constexpr int phase_mask = NNQS_PHASE_MASK;
     const bool do_hj = t->n_heavy > 0 && (phase_mask & 8);
     const int64_t row_end = row_begin + n_rows;
+    // Streams: st (caller) runs the diagonal + phase (i) and the phase (iii) kernel;
+    // hs (table-owned) the entry-driven join of the heavy alpha groups; s2 (table-owned)
+    // phase (ii), concurrently with phase (i).  Both start after everything queued on st
+    // so far and are joined back into st by events before phase (iii).
+    cudaStream_t hs = (cudaStream_t)t->own[1], s2 = (cudaStream_t)t->own[2];
+    // every buffer and event of the call; released on every exit path (stream-ordered)
+    double2 *acc_heavy = nullptr, *partial = nullptr;
+    unsigned long long *hcnt = nullptr, *ctr = nullptr;
+    u64 *hkeys = nullptr;
+    void *pbuf = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_hj = nullptr, ev_p2 = nullptr;
+    auto cleanup = [&](int code) -> int {
+        if (hkeys) cudaFreeAsync(hkeys, hs);
+        if (pbuf) cudaFreeAsync(pbuf, st);
+        if (ctr) cudaFreeAsync(ctr, st);
+        if (partial) cudaFreeAsync(partial, st);
+        if (acc_heavy) cudaFreeAsync(acc_heavy, st);
+        if (hcnt) cudaFreeAsync(hcnt, st);
+        if (ev_start) cudaEventDestroy(ev_start);
+        if (ev_hj) cudaEventDestroy(ev_hj);
+        if (ev_p2) cudaEventDestroy(ev_p2);
+        if (code) return code;
+        return cuda_check(cudaGetLastError(), "structured local energy launch");
+    };
     if (do_hj) {
-        rc = cuda_check(cudaMallocAsync((void **)&acc_heavy, 16 * n_rows + 16, st), "alloc acc_heavy");
-        if (!rc) rc = cuda_check(cudaMallocAsync((void **)&hcnt, 16, st), "alloc hj counter");
-        if (rc) return rc;
+        rc = cuda_check(nnqs_malloc_async((void **)&acc_heavy, 16 * n_rows + 16, st), "alloc acc_heavy");
+        if (!rc) rc = cuda_check(nnqs_malloc_async((void **)&hcnt, 16, st), "alloc hj counter");
+        if (rc) return cleanup(rc);
         cudaMemsetAsync(acc_heavy, 0, 16 * n_rows, st);
         cudaMemsetAsync(hcnt, 0, 16, st);
     }
-    // The entry-driven join (phase (iii) of the rows of very heavy alpha groups) runs on
-    // a second stream, concurrently with the phase (i)/(ii) kernels; the phase (iii)
-    // kernel waits for it.  hs waits for everything queued on st so far.
-    static cudaStream_t hs_of[64] = {};
-    cudaStream_t hs = st;
-    cudaEvent_t ev_start = nullptr, ev_hj = nullptr;
-    static int conc = -1;
-    if (conc < 0) {
-        const char *e = std::getenv("NNQS_HJ_CONCURRENT");
-        conc = e ? std::atoi(e) : 1;
+    rc = cuda_check(nnqs_malloc_async((void **)&partial, 32 * n_rows + 32, st), "alloc partial");
+    if (rc) return cleanup(rc);
+    double2 *partial2 = partial + n_rows + 1;
+    // longest-first row orders for the three row kernels (work estimates, one
+    // descending sort each); results do not depend on the order
+    int32_t *perm3 = nullptr, *perm20 = nullptr, *perm24 = nullptr;
+    if (t->nl_cost) {
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                                  (const int32_t *)nullptr, (int32_t *)nullptr, (int)n_rows, 0,
+                                                  32, st);
+        const size_t nb = ((size_t)4 * n_rows + 255) & ~size_t(255);
+        rc = cuda_check(nnqs_malloc_async(&pbuf, 8 * nb + tb + 256, st), "alloc row orders");
+        if (rc) return cleanup(rc);
+        char *pp = (char *)pbuf;
+        uint32_t *c3 = (uint32_t *)pp, *c20 = (uint32_t *)(pp + nb), *c24 = (uint32_t *)(pp + 2 * nb);
+        int32_t *io = (int32_t *)(pp + 3 * nb);
+        perm3 = (int32_t *)(pp + 4 * nb);
+        perm20 = (int32_t *)(pp + 5 * nb);
+        perm24 = (int32_t *)(pp + 6 * nb);
+        uint32_t *ks = (uint32_t *)(pp + 7 * nb);
+        void *tmp = pp + 8 * nb;
+        k_row_cost<<<grid_for(n_rows, 256), 256, 0, st>>>(tv, row_begin, n_rows, t->thr_double, t->thr_rowheavy,
+                                                         t->nl_cost, c3, c20, c24, io);
+        uint32_t *cs3[3] = {c3, c20, c24};
+        int32_t *ps[3] = {perm3, perm20, perm24};
+        for (int k = 0; k < 3; ++k) {
+            size_t tb1 = tb;
+            cub::DeviceRadixSort::SortPairsDescending(tmp, tb1, cs3[k], ks, io, ps[k], (int)n_rows, 0, 32, st);
+        }
     }
-    if (do_hj && conc && h->device >= 0 && h->device < 64) {
-        if (!hs_of[h->device]) cudaStreamCreateWithFlags(&hs_of[h->device], cudaStreamNonBlocking);
-        hs = hs_of[h->device];
-        cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&ev_hj, cudaEventDisableTiming);
-        cudaEventRecord(ev_start, st);
-        cudaStreamWaitEvent(hs, ev_start, 0);
+    rc = cuda_check(nnqs_malloc_async((void **)&ctr, 64, st), "alloc row counters");
+    if (rc) return cleanup(rc);
+    cudaMemsetAsync(ctr, 0, 64, st);
+    rc = cuda_check(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming), "event");
+    if (!rc) rc = cuda_check(cudaEventCreateWithFlags(&ev_hj, cudaEventDisableTiming), "event");
+    if (!rc) rc = cuda_check(cudaEventCreateWithFlags(&ev_p2, cudaEventDisableTiming), "event");
+    if (rc) return cleanup(rc);
+    cudaEventRecord(ev_start, st);        // s2 and hs start after everything queued on st
+    cudaStreamWaitEvent(s2, ev_start, 0);
+    cudaStreamWaitEvent(hs, ev_start, 0);
+    int nl = 0;
+    auto launch = [&](auto kern, const int32_t *perm, cudaStream_t ks) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+        const int gg = std::max(1, per_sm) * 148;   // persistent grid, rows from the counter
+        kern<<<gg, 256, 0, ks>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc, (unsigned long long *)stats, pairs,
+                                 phase_mask, acc_heavy, t->thr_rowheavy, partial, ctr + nl, perm, partial2, cs);
+        ++nl;
+    };
+    // three launches, each a smaller kernel (instruction cache): diagonal + phase (i)
+    // -> partial; phase (ii) (s2, concurrent) -> partial2; phase (iii) starts from
+    // partial + partial2 and finalises (fused chunk partials of Eq. (6) included)
+    launch(k_eloc_spin<3, 4, false>, perm3, st);
+    launch(k_eloc_spin<20, 4, false>, perm20, s2);
+    if (t->n_direct) {
+        launch(k_eloc_spin<3, 4, true>, perm3, st);
+        launch(k_eloc_spin<20, 4, true>, perm20, s2);
     }
-    auto run_hj = [&]() -> int {
-        int rch = NNQS_OK;
+    cudaEventRecord(ev_p2, s2);
+    cudaStreamWaitEvent(st, ev_p2, 0);
+    if (do_hj) {
+        // entry-driven join (phase (iii) of the rows of very heavy alpha groups) on hs
         int ibits = 1, rbits = 1;
         while ((1LL << ibits) < t->n) ++ibits;
         while ((1LL << rbits) < n_rows) ++rbits;
         int kbits = 1;
         while ((1LL << kbits) < h->n_groups) ++kbits;
         if (rbits + ibits + kbits > 64) kbits = 0;   // no room: k is recomputed from the strings
-        static int hj_gx = -1, hj_ev = -1;   // grid shapes (tuning: NNQS_HJ_GX, NNQS_HJ_EV)
-        if (hj_gx < 0) {
-            const char *e1 = std::getenv("NNQS_HJ_GX"), *e2 = std::getenv("NNQS_HJ_EV");
-            hj_gx = e1 ? std::atoi(e1) : 1184;
-            hj_ev = e2 ? std::atoi(e2) : 8;
-        }
-        static int hj_clip = -1;   // clip matched runs to this rank's rows (measurement knob: NNQS_HJ_CLIP)
-        if (hj_clip < 0) {
-            const char *e = std::getenv("NNQS_HJ_CLIP");
-            hj_clip = e ? std::atoi(e) : 1;
-        }
+        constexpr int hj_gx = 1184, hj_ev = 8;       // grid shapes (measured)
         const dim3 hgrid(hj_gx, t->n_heavy);
+        const int clip = (int)(row_begin > 0 || row_end < t->n);   // keep only this slice's rows
         int64_t cap = std::max<int64_t>(1 << 20, std::min<int64_t>((int64_t)1 << 26, 64 * n_rows));
-        for (int attempt = 0; attempt < 2 && !rch; ++attempt) {
+        for (int attempt = 0; attempt < 2 && !rc; ++attempt) {
             size_t tb = 0;
             cub::DeviceRadixSort::SortKeys(nullptr, tb, (const u64 *)nullptr, (u64 *)nullptr, (int)cap, kbits,
                                            kbits + ibits + rbits, hs);
-            rch = cuda_check(cudaMallocAsync((void **)&hkeys, 16 * cap + tb + 8 * n_rows + 1024, hs), "alloc hj keys");
-            if (rch) break;
+            rc = cuda_check(nnqs_malloc_async((void **)&hkeys, 16 * cap + tb + 8 * n_rows + 1024, hs), "alloc hj keys");
+            if (rc) break;
             cudaMemsetAsync(hcnt, 0, 8, hs);
-            k_hj_emit<<<hgrid, 256, 0, hs>>>(sv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end,
-                                             (int)(hj_clip && (row_begin > 0 || row_end < t->n)), ibits, kbits, hcnt,
-                                             hkeys, cap, attempt == 0 ? (unsigned long long *)stats : nullptr);
+            k_hj_emit<<<hgrid, 256, 0, hs>>>(sv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end, clip, ibits,
+                                             kbits, hcnt, hkeys, cap, attempt == 0 ? (unsigned long long *)stats : nullptr);
             unsigned long long m = 0;
-            rch = cuda_check(cudaMemcpyAsync(&m, hcnt, 8, cudaMemcpyDeviceToHost, hs), "read hj count");
-            if (!rch) rch = cuda_check(cudaStreamSynchronize(hs), "sync");
-            if (rch) break;
-            if (std::getenv("NNQS_VERBOSE"))
-                std::fprintf(stderr, "[nnqs] join: m=%llu bits=%d+%d+%d heavy_groups=%d\n", m, kbits, ibits, rbits,
-                             (int)t->n_heavy);
+            rc = cuda_check(cudaMemcpyAsync(&m, hcnt, 8, cudaMemcpyDeviceToHost, hs), "read hj count");
+            if (!rc) rc = cuda_check(cudaStreamSynchronize(hs), "sync");
+            if (rc) break;
             if ((int64_t)m > cap) {              // buffer too small: size exactly and redo
+                if (m >= (1ULL << 31)) { rc = nnqs_set_error(NNQS_E_SIZE, "entry-driven join larger than 2^31 hits"); break; }
                 cudaFreeAsync(hkeys, hs);
                 hkeys = nullptr;
                 cap = (int64_t)m;
@@ -2438,7 +2487,7 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
             if (m) {
                 u64 *k2 = hkeys + cap;
                 int32_t *kb = (int32_t *)(hkeys + 2 * cap), *ke = kb + n_rows;
-                htmp = (void *)(((uintptr_t)(ke + n_rows) + 511) & ~(uintptr_t)255);   // 256-B aligned
+                void *htmp = (void *)(((uintptr_t)(ke + n_rows) + 511) & ~(uintptr_t)255);   // 256-B aligned
                 cudaMemsetAsync(kb, 0, 8 * n_rows, hs);
                 tb = 0;
                 // order by (row, x' index) only: the group id rides along in the low bits
@@ -2451,137 +2500,14 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
             }
             break;
         }
-        if (hkeys) cudaFreeAsync(hkeys, hs);
-        hkeys = nullptr;
-        return rch;
-    };
-    double2 *partial = nullptr;
-    static int par12 = -1;   // phases (i) and (ii) on two streams (NNQS_PAR12; 0 = one chain)
-    if (par12 < 0) {
-        const char *e = std::getenv("NNQS_PAR12");
-        par12 = e ? std::atoi(e) : 1;
+        cudaEventRecord(ev_hj, hs);
+        cudaStreamWaitEvent(st, ev_hj, 0);
     }
-    static cudaStream_t s2_of[64] = {};
-    cudaStream_t s2 = nullptr;
-    if (par12 && h->device >= 0 && h->device < 64) {
-        if (!s2_of[h->device]) cudaStreamCreateWithFlags(&s2_of[h->device], cudaStreamNonBlocking);
-        s2 = s2_of[h->device];
-    }
-    rc = cuda_check(cudaMallocAsync((void **)&partial, (s2 ? 32 : 16) * n_rows + 32, st), "alloc partial");
-    double2 *partial2 = (s2 && !rc) ? partial + n_rows + 1 : nullptr;
     if (!rc) {
-        static int minb = -1;   // resident blocks/SM of the two instantiations (tuning only)
-        if (minb < 0) {
-            const char *e = std::getenv("NNQS_MINB");
-            minb = e ? std::atoi(e) : 44;
-        }
-        // longest-first row orders for the three row kernels (work estimates, one
-        // descending sort each); results do not depend on the order
-        int32_t *perm3 = nullptr, *perm20 = nullptr, *perm24 = nullptr;
-        void *pbuf = nullptr;
-        static int lpt = -1;
-        if (lpt < 0) {
-            const char *e = std::getenv("NNQS_LPT");
-            lpt = e ? std::atoi(e) : 1;
-        }
-        if (lpt && t->nl_cost) {
-            size_t tb = 0;
-            cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, (const uint32_t *)nullptr, (uint32_t *)nullptr,
-                                                      (const int32_t *)nullptr, (int32_t *)nullptr, (int)n_rows, 0,
-                                                      32, st);
-            const size_t nb = ((size_t)4 * n_rows + 255) & ~size_t(255);
-            rc = cuda_check(cudaMallocAsync(&pbuf, 8 * nb + tb + 256, st), "alloc row orders");
-            if (rc) return rc;
-            char *pp = (char *)pbuf;
-            uint32_t *c3 = (uint32_t *)pp, *c20 = (uint32_t *)(pp + nb), *c24 = (uint32_t *)(pp + 2 * nb);
-            int32_t *io = (int32_t *)(pp + 3 * nb);
-            perm3 = (int32_t *)(pp + 4 * nb);
-            perm20 = (int32_t *)(pp + 5 * nb);
-            perm24 = (int32_t *)(pp + 6 * nb);
-            uint32_t *ks = (uint32_t *)(pp + 7 * nb);
-            void *tmp = pp + 8 * nb;
-            k_row_cost<<<grid_for(n_rows, 256), 256, 0, st>>>(tv, row_begin, n_rows, t->thr_double, t->thr_rowheavy,
-                                                             t->nl_cost, c3, c20, c24, io);
-            uint32_t *cs[3] = {c3, c20, c24};
-            int32_t *ps[3] = {perm3, perm20, perm24};
-            for (int k = 0; k < 3; ++k) {
-                size_t tb1 = tb;
-                cub::DeviceRadixSort::SortPairsDescending(tmp, tb1, cs[k], ks, io, ps[k], (int)n_rows, 0, 32, st);
-            }
-        }
-        static int dyn = -1;
-        if (dyn < 0) {
-            const char *e = std::getenv("NNQS_DYN");
-            dyn = e ? std::atoi(e) : 1;
-        }
-        unsigned long long *ctr = nullptr;
-        if (dyn) {
-            rc = cuda_check(cudaMallocAsync((void **)&ctr, 64, st), "alloc row counters");
-            if (rc) return rc;
-            cudaMemsetAsync(ctr, 0, 64, st);
-        }
-        int nl = 0;
-        cudaEvent_t ev_p0 = nullptr, ev_p2 = nullptr;
-        if (s2) {   // s2 starts after everything before (row orders, counters, partial buffer)
-            cudaEventCreateWithFlags(&ev_p0, cudaEventDisableTiming);
-            cudaEventCreateWithFlags(&ev_p2, cudaEventDisableTiming);
-            cudaEventRecord(ev_p0, st);
-            cudaStreamWaitEvent(s2, ev_p0, 0);
-        }
-        auto launch = [&](auto kern, const int32_t *perm, cudaStream_t ks) {
-            int gg = g;
-            if (dyn) {
-                int per_sm = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
-                gg = std::max(1, per_sm) * 148;
-            }
-            kern<<<gg, 256, 0, ks>>>(sv, gv, tv, row_begin, n_rows, (double2 *)eloc, (unsigned long long *)stats,
-                                     pairs, phase_mask, acc_heavy, t->thr_rowheavy, partial, ctr ? ctr + nl : nullptr,
-                                     ctr ? perm : nullptr, partial2);
-            ++nl;
-        };
-        // three launches, each a smaller kernel (instruction cache): diagonal + phase (i)
-        // -> partial; phase (ii) adds; phase (iii) adds and finalises
-        // (with s2: phase (ii) on s2, concurrent with phase (i); joined before phase (iii))
-        cudaStream_t s20 = s2 ? s2 : st;
-        switch (minb / 10) {
-            case 3: launch(k_eloc_spin<3, 3, false>, perm3, st); launch(k_eloc_spin<20, 3, false>, perm20, s20); break;
-            default: launch(k_eloc_spin<3, 4, false>, perm3, st); launch(k_eloc_spin<20, 4, false>, perm20, s20);
-        }
-        if (t->n_direct) {
-            launch(k_eloc_spin<3, 4, true>, perm3, st);
-            launch(k_eloc_spin<20, 4, true>, perm20, s20);
-        }
-        if (s2) {
-            cudaEventRecord(ev_p2, s2);
-            cudaStreamWaitEvent(st, ev_p2, 0);
-        }
-        if (do_hj) {
-            rc = run_hj();
-            if (ev_hj) {
-                cudaEventRecord(ev_hj, hs);
-                cudaStreamWaitEvent(st, ev_hj, 0);
-            }
-        }
-        if (!rc) {
-            switch (minb % 10) {
-                case 3: launch(k_eloc_spin<24, 3, false>, perm24, st); break;
-                default: launch(k_eloc_spin<24, 4, false>, perm24, st);
-            }
-            if (t->n_direct) launch(k_eloc_spin<24, 4, true>, perm24, st);
-        }
-        if (ev_p0) cudaEventDestroy(ev_p0);
-        if (ev_p2) cudaEventDestroy(ev_p2);
-        if (pbuf) cudaFreeAsync(pbuf, st);
-        if (ctr) cudaFreeAsync(ctr, st);
-        cudaFreeAsync(partial, st);
+        launch(k_eloc_spin<24, 4, false>, perm24, st);
+        if (t->n_direct) launch(k_eloc_spin<24, 4, true>, perm24, st);
     }
-    if (ev_start) cudaEventDestroy(ev_start);
-    if (ev_hj) cudaEventDestroy(ev_hj);
-    if (acc_heavy) cudaFreeAsync(acc_heavy, st);
-    if (hcnt) cudaFreeAsync(hcnt, st);
-    if (rc) return rc;
-    return cuda_check(cudaGetLastError(), "structured local energy launch");
+    return cleanup(rc);
 }
 
 int nnqs_debug_counters(uint64_t *out, int reset) {

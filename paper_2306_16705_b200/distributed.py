@@ -46,46 +46,8 @@ def balanced_bounds(work, world: int, rank: int, chunk: int = REDUCE_CHUNK, n_ro
     total = sum(w)
     # floors at most half a fair share never bind (floor + work/2 <= work): the plain split
     if floor is not None and n_chunks and 2 * world * max(int(v) for v in floor) > total:
-        fl = [int(v) for v in floor]
-
-        def cost(acc, mf):   # a slice's time: its work, or its slowest row plus half its work
-            return max(acc, mf + acc // 2)
-
-        def feasible(bound):
-            k, acc, mf = 1, 0, 0
-            for c in range(n_chunks):
-                if cost(w[c], fl[c]) > bound:
-                    return False
-                if cost(acc + w[c], max(mf, fl[c])) > bound:
-                    k, acc, mf = k + 1, 0, 0
-                    if k > world:
-                        return False
-                acc += w[c]
-                mf = max(mf, fl[c])
-            return True
-
-        lo, hi = 0, max(total, max(fl)) + total
-        while lo < hi:
-            mid = (lo + hi) // 2
-            if feasible(mid):
-                hi = mid
-            else:
-                lo = mid + 1
-        # balanced fill: each rank takes at most its fair share of the remaining work
-        # and stays within the optimal bound; the last rank takes the rest
-        st, c, rem = [0], 0, total
-        for r in range(world - 1):
-            R = world - r
-            acc, mf = 0, 0
-            while c < n_chunks:
-                nacc, nmf = acc + w[c], max(mf, fl[c])
-                if acc + mf > 0 and (nacc * R > rem + R - 1 or cost(nacc, nmf) > lo):
-                    break
-                acc, mf, c = nacc, nmf, c + 1
-            rem -= acc
-            st.append(c)
-        st.append(n_chunks)
-        return min(st[rank] * chunk, n), min(st[rank + 1] * chunk, n) if rank + 1 < world else n
+        st = _floor_bounds(w, [int(v) for v in floor], world)
+        return min(st[rank] * chunk, n), (min(st[rank + 1] * chunk, n) if rank + 1 < world else n)
     if total <= 0:
         return shard_bounds(n, world, rank, chunk)
 
@@ -103,6 +65,76 @@ def balanced_bounds(work, world: int, rank: int, chunk: int = REDUCE_CHUNK, n_ro
         return n_chunks
 
     return min(start(rank) * chunk, n), min(start(rank + 1) * chunk, n)
+
+
+def _slice_cost(acc: int, mf: int) -> int:
+    """A slice's time estimate: its work, or its slowest row plus half its work."""
+    return max(acc, mf + acc // 2)
+
+
+def _reach(w, fl, bound):
+    """e[c] = the largest e with cost(w[c:e], max fl[c:e]) <= bound (e = c if chunk c alone
+    exceeds it), by two pointers with a sliding-window maximum (cost is monotone in
+    the slice), and f[c] = the fewest slices covering chunks [c, n) under the bound."""
+    from collections import deque
+    n = len(w)
+    e = [0] * n
+    dq = deque()
+    j, acc = 0, 0
+    for c in range(n):
+        if j < c:
+            j, acc = c, 0
+            dq.clear()
+        while j < n:
+            nmf = max(fl[dq[0]] if dq else 0, fl[j])
+            if _slice_cost(acc + w[j], nmf) > bound:
+                break
+            acc += w[j]
+            while dq and fl[dq[-1]] <= fl[j]:
+                dq.pop()
+            dq.append(j)
+            j += 1
+        e[c] = j
+        if j > c:
+            acc -= w[c]
+            if dq and dq[0] == c:
+                dq.popleft()
+    inf = 1 << 62          # infeasible: some chunk alone exceeds the bound
+    f = [0] * (n + 1)
+    for c in range(n - 1, -1, -1):
+        f[c] = inf if e[c] == c else min(inf, 1 + f[e[c]])
+    return e, f
+
+
+def _floor_bounds(w, fl, world):
+    """Chunk starts of `world` contiguous slices minimising the largest slice cost
+    max(work, floor + work/2): bisection on the bound with the exact min-slice count
+    (_reach), then a fill that gives every rank about its fair share of the remaining
+    work but stops early only where the rest still fits on the remaining ranks under
+    the bound (so no slice, the last included, exceeds it)."""
+    n_chunks, total = len(w), sum(w)
+    lo, hi = 0, max(total, max(fl)) + total
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if _reach(w, fl, mid)[1][0] <= world:
+            hi = mid
+        else:
+            lo = mid + 1
+    e, f = _reach(w, fl, lo)
+    st, c, rem = [0], 0, total
+    for r in range(world - 1):
+        R = world - r
+        acc = 0
+        while c < e[st[-1]] if st[-1] < n_chunks else False:
+            nacc = acc + w[c]
+            # fair share reached and the rest fits on the R - 1 other ranks: stop here
+            if acc > 0 and nacc * R > rem + R - 1 and f[c] <= R - 1:
+                break
+            acc, c = nacc, c + 1
+        rem -= acc
+        st.append(c)
+    st.append(n_chunks)
+    return st
 
 
 def all_gather_varlen(t: torch.Tensor, group=None) -> torch.Tensor:
@@ -148,11 +180,14 @@ def gather_counts(local_counts: torch.Tensor, group=None) -> torch.Tensor:
     return all_gather_varlen(local_counts.reshape(-1, 1), group).reshape(-1)
 
 
-def distributed_energy(eloc_local: torch.Tensor, counts_local: torch.Tensor, group=None, stream=None):
+def distributed_energy(eloc_local: torch.Tensor, counts_local: torch.Tensor, group=None, stream=None, p1=None):
     """Stage 4: count-weighted mean and variance (Eq. 6) over all
-    ranks' rows.  Returns a device f64[4] = (mean_re, mean_im, var, W)."""
+    ranks' rows.  p1: this rank's first-pass chunk partials if nnqs_local_energy
+    already produced them (its fused epilogue).  Returns a device f64[4] =
+    (mean_re, mean_im, var, W)."""
     from . import nnqs
-    p1 = nnqs.nnqs_energy_chunk_partials(eloc_local, counts_local, stream=stream)
+    if p1 is None:
+        p1 = nnqs.nnqs_energy_chunk_partials(eloc_local, counts_local, stream=stream)
     allp = all_gather_varlen(p1[: _n_chunks(eloc_local)], group)
     m1 = nnqs.nnqs_energy_combine(allp, 1, stream=stream)
     p2 = nnqs.nnqs_energy_chunk_partials(eloc_local, counts_local, mean_dev=m1[:2].contiguous(), stream=stream)

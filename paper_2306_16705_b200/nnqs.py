@@ -30,21 +30,29 @@ _sig = {
     "nnqs_ham_info": ([P, P, P, P, P], ctypes.c_int),
     "nnqs_ham_export": ([P, P, P, P, P], ctypes.c_int),
     "nnqs_ham_free": ([P], ctypes.c_int),
+    "nnqs_options_default": ([P], None),
     "nnqs_table_prepare": ([P, ctypes.c_int, P, P, I64, P, P], ctypes.c_int),
+    "nnqs_table_prepare_ex": ([P, ctypes.c_int, P, P, I64, P, P, P], ctypes.c_int),
+    "nnqs_table_set_algorithm": ([P, ctypes.c_int], ctypes.c_int),
     "nnqs_table_free": ([P], ctypes.c_int),
     "nnqs_table_info": ([P, P, P, P], ctypes.c_int),
-    "nnqs_local_energy": ([P, P, I64, P, P, I64, P, P, P], ctypes.c_int),
+    "nnqs_local_energy": ([P, P, I64, P, P, I64, P, P, P, P, P], ctypes.c_int),
     "nnqs_local_energy_check": ([P, I64, P], ctypes.c_int),
     "nnqs_chunk_work": ([P, I64, P, P, P], ctypes.c_int),
-    "nnqs_set_algorithm": ([ctypes.c_int], ctypes.c_int),
-    "nnqs_get_algorithm": ([], ctypes.c_int),
     "nnqs_debug_counters": ([P, ctypes.c_int], ctypes.c_int),
     "nnqs_grad_weights": ([P, P, I64, P, P, P], ctypes.c_int),
     "nnqs_energy_chunk_partials": ([P, P, I64, P, P, P], ctypes.c_int),
     "nnqs_energy_combine": ([P, I64, ctypes.c_int, P, P], ctypes.c_int),
     "nnqs_energy_reduce": ([P, P, I64, P, P], ctypes.c_int),
     "nnqs_coupled_debug": ([P, P, P, I64, I64, P, P, P, P, P, P], ctypes.c_int),
+    "nnqs_coupled_debug_rows": ([P, P, I64, I64, I64, P, P, P, P, P, P], ctypes.c_int),
 }
+class Options(ctypes.Structure):
+    """nnqs_options (include/nnqs.h): per-table algorithm and list thresholds."""
+    _fields_ = [("algorithm", ctypes.c_int32), ("thr_single", ctypes.c_int32), ("thr_double", ctypes.c_int32),
+                ("thr_rowheavy", ctypes.c_int32), ("reserved", ctypes.c_int32 * 12)]
+
+
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_lib, _name)
     _f.argtypes = _args
@@ -187,17 +195,40 @@ def nnqs_ham_from_pauli(xmask, zmask, coeff, n_qubits: int, tol: float = 0.0, de
     return Hamiltonian(out)
 
 
-def nnqs_table_prepare(ham: Hamiltonian, mode: int, keys, logpsi, stream=None) -> Table:
-    """keys: CUDA int64/uint64 [n, 2] (mode 0) or None (mode 1); logpsi CUDA float64 [n, 2]."""
+def nnqs_options_default() -> Options:
+    o = Options()
+    _lib.nnqs_options_default(ctypes.byref(o))
+    return o
+
+
+def nnqs_table_prepare(ham: Hamiltonian, mode: int, keys, logpsi, stream=None, algorithm: int | None = None,
+                       thr_single: int = 0, thr_double: int = 0, thr_rowheavy: int = 0) -> Table:
+    """keys: CUDA int64/uint64 [n, 2] (mode 0) or None (mode 1); logpsi CUDA float64 [n, 2].
+    Keyword options fill nnqs_options (0 = the library default) -> nnqs_table_prepare_ex."""
     n = int(logpsi.shape[0])
     out = P()
-    _check(_lib.nnqs_table_prepare(ham.handle, int(mode), _dev_ptr(keys), _dev_ptr(logpsi), n, _stream(stream),
-                                   ctypes.byref(out)))
+    if algorithm is None and not (thr_single or thr_double or thr_rowheavy):
+        _check(_lib.nnqs_table_prepare(ham.handle, int(mode), _dev_ptr(keys), _dev_ptr(logpsi), n, _stream(stream),
+                                       ctypes.byref(out)))
+    else:
+        o = Options()
+        o.algorithm = int(algorithm or 0)
+        o.thr_single, o.thr_double, o.thr_rowheavy = int(thr_single), int(thr_double), int(thr_rowheavy)
+        _check(_lib.nnqs_table_prepare_ex(ham.handle, int(mode), _dev_ptr(keys), _dev_ptr(logpsi), n,
+                                          ctypes.byref(o), _stream(stream), ctypes.byref(out)))
     return Table(out, mode, n)
 
 
+def nnqs_table_set_algorithm(table: Table, algorithm: int):
+    """NNQS_ALGO_AUTO (0) or NNQS_ALGO_LITERAL (1) for this table."""
+    _check(_lib.nnqs_table_set_algorithm(table.handle, int(algorithm)))
+
+
 def nnqs_local_energy(ham: Hamiltonian, table: Table, row_begin: int = 0, rows=None, row_logpsi=None,
-                      n_rows: int | None = None, eloc_out=None, stats_out=None, stream=None):
+                      n_rows: int | None = None, eloc_out=None, counts=None, partials_out=None, stats_out=None,
+                      stream=None):
+    """E_loc (device f64[n_rows][2]).  counts (device i64[n_rows]) + partials_out (device
+    f64[ceil(n_rows/1024)][3]): the fused first pass of Eq. (6) per 1024-row chunk."""
     import torch
     if n_rows is None:
         n_rows = int(rows.shape[0]) if rows is not None else table.n - row_begin
@@ -206,20 +237,12 @@ def nnqs_local_energy(ham: Hamiltonian, table: Table, row_begin: int = 0, rows=N
         device = dev.device if dev is not None else torch.device("cuda", torch.cuda.current_device())
         eloc_out = torch.empty((n_rows, 2), dtype=torch.float64, device=device)
     _check(_lib.nnqs_local_energy(ham.handle, table.handle, int(row_begin), _dev_ptr(rows), _dev_ptr(row_logpsi),
-                                  int(n_rows), _dev_ptr(eloc_out), _dev_ptr(stats_out), _stream(stream)))
+                                  int(n_rows), _dev_ptr(eloc_out), _dev_ptr(counts), _dev_ptr(partials_out),
+                                  _dev_ptr(stats_out), _stream(stream)))
     return eloc_out
 
 
 ALGO_AUTO, ALGO_LITERAL = 0, 1
-
-
-def nnqs_set_algorithm(algorithm: int):
-    """0 = auto (alpha/beta-factorised enumeration for table rows), 1 = literal loop."""
-    _check(_lib.nnqs_set_algorithm(int(algorithm)))
-
-
-def nnqs_get_algorithm() -> int:
-    return int(_lib.nnqs_get_algorithm())
 
 
 def nnqs_debug_counters(reset: bool = True):
@@ -295,6 +318,22 @@ def nnqs_coupled_debug(ham: Hamiltonian, table: Table, rows_host, max_pairs: int
     _check(_lib.nnqs_coupled_debug(ham.handle, table.handle, _np_ptr(rows_host), len(rows_host), int(max_pairs),
                                    _np_ptr(rid), _np_ptr(gid), _np_ptr(xp), _np_ptr(tix), _np_ptr(hv),
                                    ctypes.byref(n)))
+    m = n.value
+    return rid[:m], gid[:m], xp[:m], tix[:m], hv[:m]
+
+
+def nnqs_coupled_debug_rows(ham: Hamiltonian, table: Table, row_begin: int, n_rows: int, max_pairs: int = 1 << 20):
+    """Every hit the production launch sequence evaluates for table rows [row_begin, row_begin+n_rows):
+    (row table index, group id, x' key, x' table index, H_xx')."""
+    rid = np.empty(max_pairs, dtype=np.int64)
+    gid = np.empty(max_pairs, dtype=np.int64)
+    xp = np.empty((max_pairs, 2), dtype=np.uint64)
+    tix = np.empty(max_pairs, dtype=np.int64)
+    hv = np.empty(max_pairs, dtype=np.float64)
+    n = I64()
+    _check(_lib.nnqs_coupled_debug_rows(ham.handle, table.handle, int(row_begin), int(n_rows), int(max_pairs),
+                                        _np_ptr(rid), _np_ptr(gid), _np_ptr(xp), _np_ptr(tix), _np_ptr(hv),
+                                        ctypes.byref(n)))
     m = n.value
     return rid[:m], gid[:m], xp[:m], tix[:m], hv[:m]
 

@@ -27,7 +27,7 @@ from synth import configs as C  # noqa: E402
 
 
 def gpu_time(ham, tab, n, algo, reps=20):
-    nnqs.nnqs_set_algorithm(algo)
+    nnqs.nnqs_table_set_algorithm(tab, algo)
     out = torch.empty((n, 2), dtype=torch.float64, device="cuda")
     for _ in range(3):
         nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, eloc_out=out)
@@ -38,7 +38,7 @@ def gpu_time(ham, tab, n, algo, reps=20):
         nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, eloc_out=out)
     e1.record()
     e1.synchronize()
-    nnqs.nnqs_set_algorithm(nnqs.ALGO_AUTO)
+    nnqs.nnqs_table_set_algorithm(tab, nnqs.ALGO_AUTO)
     return e0.elapsed_time(e1) / reps / 1e3, out.cpu().numpy()
 
 

@@ -15,7 +15,7 @@ m = C.molecule(c); st = C.sample_table(c)
 t = time.time(); ham = nnqs.nnqs_ham_compress(m.h1, m.h2, m.n_qubits, m.e_core, device=0); print("compress", time.time() - t, ham.info())
 keys = torch.from_numpy(st.keys.view(np.int64)).to(dev); lp = torch.from_numpy(st.logpsi).to(dev)
 tab = nnqs.nnqs_table_prepare(ham, 0, keys, lp)
-nnqs.nnqs_set_algorithm(algo)
+nnqs.nnqs_table_set_algorithm(tab, algo)
 n = nrows or len(st.keys)
 out = torch.empty((n, 2), dtype=torch.float64, device=dev)
 stats = torch.zeros(4, dtype=torch.int64, device=dev)

@@ -151,6 +151,39 @@ def test_balanced_bounds_with_floor():
         [D.balanced_bounds(w, 4, r, n_rows=n) for r in range(4)]
 
 
+def test_balanced_bounds_with_floor_randomized():
+    """Floors anywhere (not only in chunk 0): the floor-aware slices never cost more than
+    the plain prefix split (max over slices of max(work, floor + work/2)), every slice
+    respects the optimal bound, slices cover the rows in order; the two cases the
+    advisor reproduced included (floor in the last / a middle chunk)."""
+    import random
+
+    def cost_of(w, fl, bs, n):
+        m = 0
+        for b, e in bs:
+            if e > b:
+                c0, c1 = b // 1024, (e + 1023) // 1024
+                acc, mf = int(sum(w[c0:c1])), int(max(fl[c0:c1]))
+                m = max(m, max(acc, mf + acc // 2))
+        return m
+
+    cases = [([14, 14, 14], [0, 0, 55], 2), ([10] * 100, [0] * 50 + [150] + [0] * 49, 8)]
+    rng = random.Random(2306)
+    for _ in range(2000):
+        nc = rng.randint(1, 40)
+        cases.append(([rng.randint(0, 30) for _ in range(nc)],
+                      [rng.choice([0, 0, 0, rng.randint(0, 300)]) for _ in range(nc)], rng.randint(1, 9)))
+    for w, fl, world in cases:
+        n = 1024 * len(w) - 3
+        bs = [D.balanced_bounds(w, world, r, n_rows=n, floor=fl) for r in range(world)]
+        assert bs[0][0] == 0 and bs[-1][1] == n
+        assert all(x[1] == y[0] and x[0] <= x[1] for x, y in zip(bs[:-1], bs[1:]))
+        plain = [D.balanced_bounds(w, world, r, n_rows=n) for r in range(world)]
+        assert cost_of(w, fl, bs, n) <= cost_of(w, fl, plain, n), (w, fl, world)
+    assert cost_of([14, 14, 14], [0, 0, 55], [D.balanced_bounds([14, 14, 14], 2, r, n_rows=3069,
+                                                                floor=[0, 0, 55]) for r in range(2)], 3069) <= 62
+
+
 def test_shard_bounds_cover_and_align():
     for n in (0, 1, 1023, 1024, 10 * 1024 + 77, 10**6):
         for world in (1, 2, 3, 4, 8):

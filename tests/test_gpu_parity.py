@@ -179,14 +179,15 @@ def test_c5_sampled_rows(nnqs, dev, c5):
 
 
 def test_c5_full_launch_sampled(nnqs, dev, c5):
-    """The bench launch: every one of the 10^6 table rows in one call; sampled
-    rows (seeded subset + HF row) checked against the oracle one by one."""
+    """The bench launch: every one of the 10^6 table rows in one call; 1024 seeded
+    rows + the HF row + the 10 longest-list rows checked against the oracle."""
     m, st, ham, tab = c5
     n = len(st.keys)
     stats = torch.zeros(4, dtype=torch.int64, device=dev)
     el = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, stats_out=stats)
     nnqs.nnqs_local_energy_check(el)
-    idx = np.unique(np.concatenate([C.oracle_row_subset(5, n, 12), [np.argmax(st.counts)]]))
+    hf, top, _ = _c5_special_rows(st)
+    idx = np.unique(np.concatenate([C.oracle_row_subset(5, n, 1024), [hf], top]))
     got = _c(el)[idx]
     ref, scale = R.eloc(m.h1, m.h2, m.e_core, st.keys[idx], st.logpsi[idx], keys=st.keys, logpsi=st.logpsi,
                         with_scale=True)
@@ -229,11 +230,11 @@ def test_c5_structured_equals_literal_hits(nnqs, dev, c5):
     s1 = torch.zeros(4, dtype=torch.int64, device=dev)
     s2 = torch.zeros(4, dtype=torch.int64, device=dev)
     a = _c(nnqs.nnqs_local_energy(ham, tab, 500_000, n_rows=4096, stats_out=s1))
-    nnqs.nnqs_set_algorithm(nnqs.ALGO_LITERAL)
+    nnqs.nnqs_table_set_algorithm(tab, nnqs.ALGO_LITERAL)
     try:
         b = _c(nnqs.nnqs_local_energy(ham, tab, 500_000, n_rows=4096, stats_out=s2))
     finally:
-        nnqs.nnqs_set_algorithm(nnqs.ALGO_AUTO)
+        nnqs.nnqs_table_set_algorithm(tab, nnqs.ALGO_AUTO)
     s1, s2 = s1.cpu().numpy(), s2.cpu().numpy()
     assert s1[2] == s2[2] and s1[3] < s2[3]
     assert np.max(np.abs(a - b) / np.maximum(np.abs(b), 1.0)) < 1e-9
@@ -263,6 +264,183 @@ def test_coupled_configurations_bit_exact(nnqs, dev, c, variant):
         for k, v in want.items():
             assert np.sign(got[k]) == np.sign(v)
             assert abs(got[k] - v) <= 1e-12 * max(1.0, abs(v))
+
+
+# ------------------------------- P3 on the production (structured) path
+def _oracle_hits(m, keys, rows_idx, workers=16):
+    """oracle row_hits (plain term-by-term Eq. 9 + bisection) of many rows, threaded
+    (the ctypes call releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(workers) as ex:
+        return list(ex.map(lambda i: R.row_hits(m.h1, m.h2, m.e_core, keys[i], keys=keys), rows_idx))
+
+
+def _p3_compare(m, keys, i, rid, gid, xp, tix, hv, ref):
+    """Bit-exact P3 for one row: the set of x' (table indices) with |H| > tau equals the
+    oracle's, every logged x' is x ^ X_k for a group k of the table and is logged once,
+    signs agree, values agree to rounding; extras have |H| <= tau (structural zeros)."""
+    tau = 1e-13 * max(np.abs(m.h1).max(), np.abs(m.h2).max())
+    ridx, rh = ref
+    assert (rid == i).all()
+    assert len(np.unique(tix)) == len(tix), f"row {i}: an x' evaluated twice"
+    assert (gid >= 0).all(), f"row {i}: x ^ x' is not a flip group of the table"
+    assert np.array_equal(xp, keys[tix])
+    want = {int(a): b for a, b in zip(ridx, rh) if abs(b) > tau}
+    got = dict(zip(tix.tolist(), hv.tolist()))
+    assert set(k for k, v in got.items() if abs(v) > tau) == set(want), f"row {i}: hit sets differ"
+    for k, v in want.items():
+        assert np.sign(got[k]) == np.sign(v), f"row {i}, x' {k}: sign"
+        assert abs(got[k] - v) <= 1e-12 * max(1.0, abs(v)), f"row {i}, x' {k}: {got[k]} vs {v}"
+
+
+def _p3_check(nnqs, ham, tab, m, keys, rows_idx, per_row=False):
+    rows_idx = np.asarray(rows_idx)
+    refs = _oracle_hits(m, keys, rows_idx)
+    if per_row:        # one production call per row (large rows: the C5 HF row has ~44k hits)
+        for i, ref in zip(rows_idx, refs):
+            rid, gid, xp, tix, hv = nnqs.nnqs_coupled_debug_rows(ham, tab, int(i), 1, max_pairs=1 << 18)
+            _p3_compare(m, keys, int(i), rid, gid, xp, tix, hv, ref)
+        return
+    # one production call over the whole row range, hits grouped by row
+    lo, hi = int(rows_idx.min()), int(rows_idx.max()) + 1
+    rid, gid, xp, tix, hv = nnqs.nnqs_coupled_debug_rows(ham, tab, lo, hi - lo, max_pairs=1 << 23)
+    order = np.argsort(rid, kind="stable")
+    rid, gid, xp, tix, hv = rid[order], gid[order], xp[order], tix[order], hv[order]
+    starts = np.searchsorted(rid, rows_idx, "left")
+    ends = np.searchsorted(rid, rows_idx, "right")
+    for i, a, b, ref in zip(rows_idx, starts, ends, refs):
+        _p3_compare(m, keys, int(i), rid[a:b], gid[a:b], xp[a:b], tix[a:b], hv[a:b], ref)
+
+
+@pytest.mark.parametrize("c,variant", [(2, "full"), (2, "half"), (3, "full"), (3, "half"), (4, "full")])
+def test_production_coupled_configurations_bit_exact(nnqs, dev, c, variant):
+    """P3 on the path nnqs_local_energy runs for table rows (the structured kernels):
+    every row of the table, its (x', lookup index) set and signs bit-exact against the
+    oracle (Algorithm 2's hit/sign steps)."""
+    m = C.molecule(c)
+    st = C.sample_table(c, variant)
+    ham = ham_for(nnqs, c)
+    tab = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(st.logpsi, dev))
+    _p3_check(nnqs, ham, tab, m, st.keys, np.arange(len(st.keys)))
+
+
+def _c5_special_rows(st):
+    """The HF row (largest count) and the 10 rows with the longest alpha + beta lists
+    (the rows with the most hits), plus 100 seeded rows (SURVEY.md 8(c) reading 20)."""
+    from synth import samples as SS  # noqa: F401
+    k = st.keys
+
+    def spin(w, s):
+        w = (w >> np.uint64(s)) & np.uint64(0x5555555555555555)
+        for sh, mk in [(1, 0x3333333333333333), (2, 0x0F0F0F0F0F0F0F0F), (4, 0x00FF00FF00FF00FF),
+                       (8, 0x0000FFFF0000FFFF), (16, 0x00000000FFFFFFFF)]:
+            w = (w | (w >> np.uint64(sh))) & np.uint64(mk)
+        return w
+    a = spin(k[:, 0], 0) | (spin(k[:, 1], 0) << np.uint64(32))
+    b = spin(k[:, 0], 1) | (spin(k[:, 1], 1) << np.uint64(32))
+    _, ia, ca = np.unique(a, return_inverse=True, return_counts=True)
+    _, ib, cb = np.unique(b, return_inverse=True, return_counts=True)
+    size = ca[ia] + cb[ib]
+    hf = int(np.argmax(st.counts))
+    top = [int(i) for i in np.argsort(-size, kind="stable") if i != hf][:10]
+    seeded = C.oracle_row_subset(5, len(k), 100)
+    return hf, top, seeded
+
+
+def test_c5_production_coupled_configurations_bit_exact(nnqs, dev, c5):
+    """P3 at the headline config on the production path: the HF row (~44k hits, the
+    entry-driven join + multimap probes), the 10 rows with the longest lists and 100
+    seeded rows -- x' sets, lookup indices and signs bit-exact against the oracle."""
+    m, st, ham, tab = c5
+    hf, top, seeded = _c5_special_rows(st)
+    _p3_check(nnqs, ham, tab, m, st.keys, [hf] + top, per_row=True)
+    _p3_check(nnqs, ham, tab, m, st.keys, seeded, per_row=True)
+
+
+def test_structured_zero_psi_rows(nnqs, dev):
+    """psi(x) = 0 (log psi = -inf) on the structured path (reading R10): those rows are
+    NaN (NNQS_E_ZERO_PSI from the check), and as x' of other rows they contribute 0;
+    every other row matches the oracle."""
+    for c in (3, 4):
+        m = C.molecule(c)
+        st = C.sample_table(c, "full")
+        lp = st.logpsi.copy()
+        rng = np.random.default_rng(77 + c)
+        zero = np.sort(rng.choice(len(lp), size=max(3, len(lp) // 50), replace=False))
+        lp[zero, 0] = -np.inf
+        ham = ham_for(nnqs, c)
+        tab = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(lp, dev))
+        el = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=len(lp))
+        with pytest.raises(nnqs.NNQSError) as e:
+            nnqs.nnqs_local_energy_check(el)
+        assert e.value.code == nnqs.NNQS_E_ZERO_PSI
+        got = _c(el)
+        assert np.isnan(got[zero]).all()
+        ok = np.setdiff1d(np.arange(len(lp)), zero)
+        ref, scale = R.eloc(m.h1, m.h2, m.e_core, st.keys[ok], lp[ok], keys=st.keys, logpsi=lp, with_scale=True)
+        _assert_close(got[ok], ref, scale, f"C{c} zero-psi")
+
+
+@pytest.mark.parametrize("c", [3, 4])
+def test_fused_chunk_partials(nnqs, dev, c):
+    """nnqs_local_energy(counts, partials_out): the fused first pass of Eq. (6) equals
+    nnqs_energy_chunk_partials bit for bit, on both algorithms and on a chunk-aligned
+    slice; the partials of the slices combine to the single-call energy bit for bit."""
+    st = C.sample_table(c, "full")
+    ham = ham_for(nnqs, c)
+    n = len(st.keys)
+    cnt = _t(st.counts, dev)
+    for algo in (nnqs.ALGO_AUTO, nnqs.ALGO_LITERAL):
+        tab = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(st.logpsi, dev), algorithm=algo)
+        nch = (n + 1023) // 1024
+        part = torch.full((nch, 3), np.nan, dtype=torch.float64, device=dev)
+        el = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, counts=cnt, partials_out=part)
+        ref = nnqs.nnqs_energy_chunk_partials(el, cnt)
+        assert part.cpu().numpy().tobytes() == ref.cpu().numpy().tobytes()
+        if n > 2048:
+            cut = 1024 * (nch // 2)
+            p1 = torch.empty(((cut + 1023) // 1024, 3), dtype=torch.float64, device=dev)
+            p2 = torch.empty(((n - cut + 1023) // 1024, 3), dtype=torch.float64, device=dev)
+            nnqs.nnqs_local_energy(ham, tab, 0, n_rows=cut, counts=cnt[:cut], partials_out=p1)
+            nnqs.nnqs_local_energy(ham, tab, cut, n_rows=n - cut, counts=cnt[cut:], partials_out=p2)
+            a = nnqs.nnqs_energy_combine(torch.cat([p1, p2]), 1).cpu().numpy()
+            b = nnqs.nnqs_energy_combine(ref, 1).cpu().numpy()
+            assert a.tobytes() == b.tobytes()
+
+
+def test_c5_fixture_every_row(nnqs, dev, c5):
+    """Every-row parity at the headline config (SURVEY.md 8(c) reading 20): all 10^6
+    E_loc against the committed oracle fixture (scripts/c5_oracle_fixture.py, oracle/
+    only), and Eq. (6) mean / variance against the oracle's (R14 tolerances)."""
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "c5_eloc.npz")
+    if not os.path.exists(path):
+        pytest.skip("C5 oracle fixture not generated (scripts/c5_oracle_fixture.py)")
+    m, st, ham, tab = c5
+    z = np.load(path)
+    import hashlib
+    h = hashlib.sha256()
+    for a in (st.keys, st.counts, st.logpsi):
+        h.update(np.ascontiguousarray(a).tobytes())
+    assert str(z["digest"]) == h.hexdigest(), "fixture computed from other C5 inputs"
+    n = len(st.keys)
+    cnt = _t(st.counts, dev)
+    part = torch.empty(((n + 1023) // 1024, 3), dtype=torch.float64, device=dev)
+    el = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, counts=cnt, partials_out=part)
+    got = _c(el)
+    have = z["have"]
+    assert have.sum() > 0
+    ref = z["re"][have] + 1j * z["im"][have]
+    _assert_close(got[have], ref, z["scale"][have], f"C5 fixture ({int(have.sum())} rows)")
+    if bool(z["complete"]):
+        m1 = nnqs.nnqs_energy_combine(part, 1)
+        m2 = nnqs.nnqs_energy_combine(nnqs.nnqs_energy_chunk_partials(el, cnt, mean_dev=m1[:2].contiguous()), 2)
+        m1, m2 = m1.cpu().numpy(), m2.cpu().numpy()
+        TOLE = TOL * float(z["energy_scale"])
+        assert abs(m1[0] - float(z["mean_re"])) <= TOLE and abs(m1[1] - float(z["mean_im"])) <= TOLE
+        var = float(z["var"])
+        assert abs(m2[0] - var) <= TOL * var + 2 * TOL * np.sqrt(var) * float(z["max_abs"])
+        assert m1[2] == float(z["W"])
 
 
 # ---------------------------------------------------- Pauli-level semantics
@@ -354,11 +532,8 @@ def test_structured_equals_literal(nnqs, dev, c, variant):
     s1 = torch.zeros(4, dtype=torch.int64, device=dev)
     s2 = torch.zeros(4, dtype=torch.int64, device=dev)
     a = _c(nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, stats_out=s1))
-    nnqs.nnqs_set_algorithm(nnqs.ALGO_LITERAL)
-    try:
-        b = _c(nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, stats_out=s2))
-    finally:
-        nnqs.nnqs_set_algorithm(nnqs.ALGO_AUTO)
+    lit = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(st.logpsi, dev), algorithm=nnqs.ALGO_LITERAL)
+    b = _c(nnqs.nnqs_local_energy(ham, lit, 0, n_rows=n, stats_out=s2))
     s1, s2 = s1.cpu().numpy(), s2.cpu().numpy()
     assert s1[0] == s2[0] == n * ham.info()["n_groups"]
     assert s1[2] == s2[2]                       # identical hit sets (counts)
@@ -429,11 +604,11 @@ def test_chunk_work_and_balanced_slices(nnqs, dev):
     with pytest.raises(nnqs.NNQSError) as e:
         nnqs.nnqs_chunk_work(tab, chunk=0)
     assert e.value.code == nnqs.NNQS_E_ARG
-    nnqs.nnqs_set_algorithm(1)
+    nnqs.nnqs_table_set_algorithm(tab, nnqs.ALGO_LITERAL)
     try:
         lit = nnqs.nnqs_chunk_work(tab)
     finally:
-        nnqs.nnqs_set_algorithm(0)
+        nnqs.nnqs_table_set_algorithm(tab, nnqs.ALGO_AUTO)
     assert lit.sum() == n and (lit[:-1] == 1024).all()
     cnt = _t(st.counts, dev)
     full = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n)
@@ -481,17 +656,14 @@ def test_grad_weights_matches_oracle(nnqs, dev):
 
 
 @pytest.mark.parametrize("mixed,rowheavy", [(False, 40), (False, 1000), (True, 1000)])
-def test_structured_heavy_paths_small(nnqs, dev, mixed, rowheavy, monkeypatch):
+def test_structured_heavy_paths_small(nnqs, dev, mixed, rowheavy):
     """The heavy-group machinery (deletion multimap with its Bloom filter, the
     compact-key or two-sort build, heavy-neighbour probes, the entry-driven join)
-    forced onto C4 by low thresholds (NNQS_THR_* are read at table build):
+    forced onto C4 by low thresholds (per-table nnqs_options):
     rowheavy=40 sends every row's phase (iii) through the join, 1000 through the
     row kernel's probes; mixed=True holds two particle sectors (two-sort build,
     no single-sector shortcut).  Two rows get psi(x) < e^-600 (DIRECT kernels).
     E_loc of sampled rows against the oracle."""
-    monkeypatch.setenv("NNQS_THR_SINGLE", "3")
-    monkeypatch.setenv("NNQS_THR_DOUBLE", "6")
-    monkeypatch.setenv("NNQS_THR_ROWHEAVY", str(rowheavy))
     m = C.molecule(4)
     keys = S.sector_keys(10, 7, 7)
     if mixed:
@@ -502,7 +674,8 @@ def test_structured_heavy_paths_small(nnqs, dev, mixed, rowheavy, monkeypatch):
     lp = np.stack([rng.normal(0, 1, len(keys)), rng.uniform(-np.pi, np.pi, len(keys))], axis=1)
     lp[[3, 1000], 0] -= 620.0                                  # DIRECT rows (reading R11)
     ham = ham_for(nnqs, 4)
-    tab = nnqs.nnqs_table_prepare(ham, 0, _t(keys, dev), _t(lp, dev))
+    tab = nnqs.nnqs_table_prepare(ham, 0, _t(keys, dev), _t(lp, dev), thr_single=3, thr_double=6,
+                                  thr_rowheavy=rowheavy)
     n = len(keys)
     stats = torch.zeros(4, dtype=torch.int64, device=dev)
     got = _c(nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, stats_out=stats))
@@ -510,12 +683,10 @@ def test_structured_heavy_paths_small(nnqs, dev, mixed, rowheavy, monkeypatch):
     ref, scale = R.eloc(m.h1, m.h2, m.e_core, keys[sel], lp[sel], keys=keys, logpsi=lp, with_scale=True)
     _assert_close(got[sel], ref, scale, f"heavy paths mixed={mixed}")
     s2 = torch.zeros(4, dtype=torch.int64, device=dev)
-    nnqs.nnqs_set_algorithm(nnqs.ALGO_LITERAL)
-    try:
-        nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, stats_out=s2)
-    finally:
-        nnqs.nnqs_set_algorithm(nnqs.ALGO_AUTO)
-    assert stats.cpu().numpy()[2] == s2.cpu().numpy()[2]     # identical hit sets
+    lit = nnqs.nnqs_table_prepare(ham, 0, _t(keys, dev), _t(lp, dev), algorithm=nnqs.ALGO_LITERAL)
+    nnqs.nnqs_local_energy(ham, lit, 0, n_rows=n, stats_out=s2)
+    assert stats.cpu().numpy()[2] == s2.cpu().numpy()[2]     # identical hit counts
+    _p3_check(nnqs, ham, tab, m, keys, np.arange(0, n, max(1, n // 40)))   # and identical hit sets
     # degenerate slices through the same machinery: empty, one row, the last row
     assert nnqs.nnqs_local_energy(ham, tab, 7, n_rows=0).shape[0] == 0
     full = nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n).cpu().numpy()
