@@ -1,10 +1,9 @@
 #!/bin/bash
-# round-2 GPU session A: parity suite, smoke, bench, sanitizers
+# round-2 GPU session A: parity suite, smoke, bench, launch list
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_r2a.log 2>&1
 timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu_r2a.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_r2a.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r2a.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r2a.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_r2a.log
 timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_r2a.json 2> gpurun_out/bench_r2a.err
-for tool in memcheck synccheck racecheck; do
-  timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/sanitize_run.py --c5 > gpurun_out/san_$tool.txt 2>&1; echo "rc=$?" >> gpurun_out/san_$tool.txt
-done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r2a.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/b_ncu_r2a.log 2>&1
