@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--config", default="C5", choices=["C4", "C5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=0, help="oracle sample rows (0 = auto)")
+    ap.add_argument("--ncu", default="auto", choices=["auto", "off"],
+                    help="profile one local-energy call with ncu in this run (DRAM bytes, ALU-pipe %%)")
     return ap.parse_args()
 
 
@@ -77,28 +79,64 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml(self):
+        """In-process NVML (the library behind nvidia-smi): a sample costs microseconds,
+        so sampling does not perturb the timed steps; None if unavailable."""
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            bits = {"hw_slowdown": pynvml.nvmlClocksThrottleReasonHwSlowdown,
+                    "hw_thermal_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                    "sw_thermal_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                    "sw_power_cap": pynvml.nvmlClocksThrottleReasonSwPowerCap}
+
+            def sample():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                return [str(sm), str(mx), hex(rs)] + ["Active" if rs & b else "Not Active" for b in bits.values()]
+            sample()
+            return sample
+        except Exception:
+            return None
+
     def _run(self):
+        sample = self._nvml()
+        self.source = "nvml" if sample else "nvidia-smi"
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([s.strip() for s in out.split(",")])
+                if sample:
+                    self.rows.append(sample())
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([s.strip() for s in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._ready.set()
+            self._stop.wait(0.05 if sample else 0.2)
 
     def __enter__(self):
+        self._ready = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        self._ready.wait(10)          # first sample taken before the timed region starts
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
 
+    def mark(self):
+        """Start of the timed region: summary() keeps the samples taken after it."""
+        self._first = len(self.rows)
+
     def summary(self):
+        if getattr(self, "_first", 0):
+            self.rows = self.rows[self._first:]
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
@@ -110,7 +148,7 @@ class ClockSampler:
                 if v.strip().lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+                "reasons": sorted(reasons), "samples": len(self.rows), "source": getattr(self, "source", None)}
 
 
 def peaks():
@@ -136,6 +174,76 @@ def alu_peak_ops(sm_mhz):
                                               f"{d['popc_tops']:.2f}, IADD {d['iadd_tops']:.2f} Tops/s)")
     except Exception:
         return 148 * 64 * sm_mhz * 1e6, (f"derived: 148 SMs x 64 INT32 lanes/clk (alu pipe) x {sm_mhz:.0f} MHz")
+
+
+PROBE_PEAKS_FILE = os.path.join(ROOT, "profiles", "r02_probe_peaks.json")
+
+
+def probe_peak():
+    """Random 32-B probe roof (scripts/microbench/probe_peaks.cu on this pool's
+    B200): independent random sector loads per second with an L2-resident
+    working set (the psi_hat / coefficient tables the hits read); the HBM figure
+    is reported beside it.  Returns (probes/s, hbm probes/s, source) or Nones."""
+    try:
+        d = json.load(open(PROBE_PEAKS_FILE))
+        l2 = max(float(v) for k, v in d["indep"].items() if int(k[:-2]) <= 64)
+        hbm = float(d["indep"]["4096MB"])
+        return l2, hbm, (f"measured: random independent 32-B loads, {l2:.3g}/s L2-resident (<= 64 MB), "
+                         f"{hbm:.3g}/s over 4 GB (HBM) ({os.path.relpath(PROBE_PEAKS_FILE, ROOT)})")
+    except Exception:
+        return None, None, "unavailable"
+
+
+NCU_METRICS = ("gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,"
+               "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active")
+
+
+def live_ncu(config_c, timeout_s=420):
+    """ncu over ONE nnqs_local_energy call of this workload (scripts/ncu_one_call.py),
+    run by this bench invocation after its timed region: per kernel of the call
+    the duration (cold, serialised), DRAM bytes, L2 hit rate and ALU-pipe issue %.
+    Returns a dict or None (ncu missing / failed)."""
+    import shutil
+    import subprocess
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None
+    log = os.path.join("/tmp", f"nnqs_bench_ncu_{os.getpid()}.csv")
+    cmd = [ncu, "--metrics", NCU_METRICS, "--clock-control", "none", "-k", "regex:k_eloc_spin|k_hj|k_p3h",
+           "--csv", "--log-file", log, sys.executable, os.path.join(ROOT, "scripts", "ncu_one_call.py"),
+           str(config_c)]
+    try:
+        r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout_s)
+        if r.returncode != 0 or not os.path.exists(log):
+            return None
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        from ncu_metrics import load
+        per = load(log)
+    except Exception:
+        return None
+    finally:
+        try:
+            os.remove(log)
+        except OSError:
+            pass
+    if not per:
+        return None
+    tot_b = sum(d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0) for d in per.values())
+    tt = sum(d.get("gpu__time_duration.sum", 0) for d in per.values())
+    alu_w = sum(d.get("gpu__time_duration.sum", 0) *
+                d.get("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", 0) for d in per.values())
+    return {"bytes_per_launch": tot_b, "kernels": sorted(per),
+            "source": "ncu in this bench run: one nnqs_local_energy call (scripts/ncu_one_call.py), "
+                      "--clock-control none, cold and serialised",
+            "ncu_alu_pipe_pct_time_weighted": alu_w / tt if tt else None,
+            "per_kernel": {k: {"ms": round(d.get("gpu__time_duration.sum", 0) / 1e6, 3),
+                               "dram_gb": round((d.get("dram__bytes_read.sum", 0) +
+                                                 d.get("dram__bytes_write.sum", 0)) / 1e9, 3),
+                               "l2_hit_pct": round(d.get("lts__t_sector_hit_rate.pct", 0), 1),
+                               "alu_pipe_pct": round(d.get(
+                                   "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", 0), 1)}
+                           for k, d in per.items()},
+            "kernels_ms_serialised": tt / 1e6}
 
 
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_local_energy_full.txt")
@@ -339,7 +447,9 @@ def run_ours(args):
             en = torch.stack([m1[0], m1[1], m2[0], m1[2]])
         return tab, en
 
-    for _ in range(args.warmup):
+    clk = ClockSampler(local).__enter__()   # sampling from before the warm-up: no thread start in the timed region
+    for _ in range(args.warmup):       # the same work as a timed step (L2 flush included)
+        flush.fill_(1)
         tab, en = step(keys_d, lp_d, cnt_d, False)
         tab.close()
     torch.cuda.synchronize()
@@ -350,7 +460,8 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    clk.mark()
+    if True:
         for _ in range(args.steps):
             flush.fill_(1)
             a0 = torch.cuda.Event(enable_timing=True)
@@ -362,6 +473,7 @@ def run_ours(args):
             step_ms.append(a0.elapsed_time(a1))
             tab.close()
         torch.cuda.synchronize()
+    clk.__exit__()
     if world > 1:
         dist.barrier()
     t_total = sum(step_ms) / 1e3
@@ -434,7 +546,13 @@ def run_ours(args):
     if world > 1:
         ops_launch = ops_launch // world
     achieved = ops_launch / (kern_avg_ms / 1e3)
-    per_launch_traffic = profile_traffic()
+    live = live_ncu(c) if (args.ncu == "auto" and world == 1) else None
+    per_launch_traffic = live or profile_traffic()
+    # probe roof: every hit needs two dependent random reads
+    # (psi_hat(x') and its coefficient H_xx'); rows and lists stream
+    p_l2, p_hbm, p_src = probe_peak()
+    probes_launch = 2 * int(st_local[2]) // max(world, 1)
+    probe_rate = probes_launch / (kern_avg_ms / 1e3)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True,
@@ -458,10 +576,23 @@ def run_ours(args):
             "candidates_examined": int(st_local[1]) / max(world, 1) / (kern_avg_ms / 1e3),
             "hits": int(st_local[2]) / max(world, 1) / (kern_avg_ms / 1e3),
             "terms_evaluated": int(st_local[3]) / max(world, 1) / (kern_avg_ms / 1e3)},
-        "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": alu_peak / 1e12,
-                     "unit": "Tops/s (INT32 ALU-pipe)", "frac": achieved / alu_peak, "traffic": per_launch_traffic,
-                     "kernel": "nnqs_local_energy, structured path: k_hj_emit + CUB sort + k_hj_eval + "
-                               "k_eloc_spin x4 (one launch sequence, timed with CUDA events on its stream)",
+        "roofline": {"bound": "probe", "achieved": probe_rate, "peak": p_l2,
+                     "unit": "random 32-B probes/s",
+                     "frac": (probe_rate / p_l2) if p_l2 else None,
+                     "traffic": per_launch_traffic["bytes_per_launch"] if per_launch_traffic else None,
+                     "traffic_detail": per_launch_traffic,
+                     "kernel": "nnqs_local_energy, structured path: k_eloc_spin<3>/<20>/<24> + k_hj_* "
+                               "(one launch sequence, timed with CUDA events on its stream)",
+                     "peak_source": p_src,
+                     "probes_per_launch": probes_launch,
+                     "probes_definition": "2 dependent random reads per hit (psi_hat(x') and the coefficient of "
+                                          "H_xx'; PAPER.md:406-421), hits from the kernel counters",
+                     "hbm_probe_peak": p_hbm,
+                     "dram_gbs": (per_launch_traffic["bytes_per_launch"] / (kern_avg_ms / 1e3) / 1e9)
+                     if per_launch_traffic else None,
+                     "hbm_peak_gbs": float(pk.get("hbm_gbs", 6650.0))},
+        "roofline_alu": {"bound": "alu", "achieved": achieved / 1e12, "peak": alu_peak / 1e12,
+                     "unit": "Tops/s (INT32 ALU-pipe)", "frac": achieved / alu_peak,
                      "peak_source": alu_src,
                      "algorithmic_ops_per_launch": ops_launch,
                      "issue_utilisation": None if not per_launch_traffic else {
@@ -469,7 +600,8 @@ def run_ours(args):
                                  "time-weighted over the local-energy call; frac above is the algorithmic "
                                  "fraction (8(d)(ii)) reported beside it",
                          "alu_pipe_pct_time_weighted": per_launch_traffic["ncu_alu_pipe_pct_time_weighted"],
-                         "alu_pipe_pct": per_launch_traffic["ncu_alu_pipe_pct"],
+                         "alu_pipe_pct": per_launch_traffic.get("ncu_alu_pipe_pct") or
+                         {k: v["alu_pipe_pct"] for k, v in per_launch_traffic.get("per_kernel", {}).items()},
                          "source": per_launch_traffic["source"]},
                      "ops_definition": "4 x candidates examined + 6 x (folded) Pauli strings evaluated "
                                        "(kernel counters); the kernel is bound by dependent random-access "

@@ -72,6 +72,17 @@ struct SpinIndex {
     // slot (spin * P + pair rank): {B.lo, B.hi (as bits), T, 0, c_0 .. c_{N-1}}.
     bool occ_ok = false;
     std::vector<double> occ_rec;      // [2P][4 + N]
+    // Alpha pair x beta pair groups in closed form: every such group folds to one
+    // string Z = canon(J), J = JW(2p, 2q) ^ JW(2r+1, 2s+1) (the qubits strictly
+    // between each pair's sites), so its value at an in-sector x is
+    // ab_d[U * P + V] * (-1)^{popc(x & J)} (U, V the pair ranks; the canonical
+    // representative's flips are folded into ab_d).  Existence bit per slot.
+    bool ab_ok = false;
+    int64_t ab_w = 0;                 // 64-bit words per U row of ab_bits
+    std::vector<double> ab_d;         // [P*P]
+    std::vector<u64> ab_bits;         // [P * ab_w]
+    std::vector<uint32_t> pair_sites; // [P] p | q << 8 (p < q) of pair rank U
+    std::vector<u64> pair_J;          // [2][P][2] JW string masks: alpha pair U, beta pair V
     std::vector<uint32_t> foff;       // [K+1]
     std::vector<u64> fz;              // [M][2]
     std::vector<double> fd;           // [M]
@@ -96,6 +107,9 @@ struct DeviceHam {
     int32_t *quad_rec[2] = {nullptr, nullptr};
     int32_t *ab_k = nullptr;
     int32_t *ab_rec = nullptr;
+    double *ab_d = nullptr;    // alpha x beta groups in closed form (SpinIndex::ab_ok)
+    u64 *ab_bits = nullptr;
+    u64 *pair_J = nullptr;
     double *diag_uv = nullptr; // diagonal group in occupation form (structured path)
     double *occ_rec = nullptr; // single-excitation groups in occupation form
     void *frng = nullptr;      // folded table (structured path): uint2 range per group,

@@ -24,6 +24,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <mutex>
+#include <limits>
 #include <cstdlib>
 #include <cstring>
 
@@ -76,6 +78,44 @@ __host__ __device__ __forceinline__ u64 mix64(u64 z) {
     return z ^ (z >> 31);
 }
 
+
+// L2 eviction-priority hints (PTX createpolicy + ld.global.nc.L2::cache_hint):
+// the multimap's slots and records are touched once per probe and spread over
+// GBs -- marked evict-first so that they do not push the small, reused tables
+// (Bloom words, psi_hat, string lists, folded strings) out of the 126-MB L2.
+#ifndef NNQS_L2HINT
+#define NNQS_L2HINT 0
+#endif
+__device__ __forceinline__ u64 pol_stream() {
+    u64 p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ u64 pol_keep() {
+    u64 p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ ulonglong2 ld_hint(const ulonglong2 *ptr, u64 pol) {
+    ulonglong2 v;
+    asm("ld.global.nc.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;" : "=l"(v.x), "=l"(v.y) : "l"(ptr), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ ulonglong2 ld_stream(const ulonglong2 *ptr) {
+#if NNQS_L2HINT & 1
+    return ld_hint(ptr, pol_stream());
+#else
+    return __ldg(ptr);
+#endif
+}
+__device__ __forceinline__ ulonglong2 ld_keep(const ulonglong2 *ptr) {
+#if NNQS_L2HINT & 2
+    return ld_hint(ptr, pol_keep());
+#else
+    return __ldg(ptr);
+#endif
+}
+
 // ------------------------------------------------------------- device views
 struct SpinView {
     int n;
@@ -88,7 +128,32 @@ struct SpinView {
     const double *occ_rec;    // single-excitation records (SpinIndex::occ_rec) or nullptr
     double diag_K;            // diagonal group in occupation form (SpinIndex), or
     const double *diag_uv;    // nullptr: evaluate its Pauli strings
+    const double *ab_d;       // alpha x beta groups in closed form (SpinIndex::ab_ok), or nullptr
+    const u64 *ab_bits;       //   existence bit per (U, V) slot, rows of ab_w words
+    int64_t ab_w;
+    const ulonglong2 *pair_J;     // [2][P] JW string masks of alpha / beta pairs
 };
+
+// x' = x ^ X with X = alpha pair U (qubits 2p, 2q) x beta pair V (2r+1, 2s+1):
+// H_{x'x} = ab_d[U P + V] (-1)^{popc(x & J)}, J = the qubits strictly between
+// each pair's sites (the JW strings; SpinIndex::ab_d).
+__device__ __forceinline__ double ab_value(const double *ab_d, const ulonglong2 *pair_J, int64_t P, uint32_t U,
+                                           uint32_t V, u64 x0, u64 x1) {
+    const ulonglong2 ja = __ldg(pair_J + U), jb = __ldg(pair_J + P + V);   // JW strings of the two pairs
+    const u64 m0 = ja.x ^ jb.x, m1 = ja.y ^ jb.y;
+    const double d = __ldg(ab_d + (int64_t)U * P + V);
+    return __longlong_as_double(__double_as_longlong(d) ^
+                                ((long long)((__popcll(x0 & m0) + __popcll(x1 & m1)) & 1) << 63));
+}
+// existence of the alpha x beta group (U, V): its queue key AB_TAG | U << 11 | V, or -1
+#define AB_TAG 0x20000000
+__device__ __forceinline__ int32_t ab_key(const SpinView &S, int32_t U, int32_t V) {
+    if (S.ab_d) {
+        const u64 w = __ldg(S.ab_bits + (int64_t)U * S.ab_w + (V >> 6));
+        return ((w >> (V & 63)) & 1) ? (int32_t)(AB_TAG | (U << 11) | V) : -1;
+    }
+    return __ldg(S.ab_rec + (int64_t)U * S.P + V);
+}
 
 // folded table on the device: per group its string range, per string one 32-B
 // record {Z lo, Z hi}, {d bits, 0} (one sector per string instead of two)
@@ -97,9 +162,9 @@ struct GroupView {
     const ulonglong2 *rec;
 };
 __device__ __forceinline__ uint2 g_range(const GroupView &G, int32_t k) { return __ldg(G.grng + k); }
-__device__ __forceinline__ ulonglong2 g_z(const GroupView &G, uint32_t i) { return __ldg(G.rec + 2 * i); }
+__device__ __forceinline__ ulonglong2 g_z(const GroupView &G, uint32_t i) { return ld_keep(G.rec + 2 * i); }
 __device__ __forceinline__ double g_d(const GroupView &G, uint32_t i) {
-    return __longlong_as_double((long long)__ldg(G.rec + 2 * i + 1).x);
+    return __longlong_as_double((long long)ld_keep(G.rec + 2 * i + 1).x);
 }
 
 // Parity/debug hit log (nnqs_coupled_debug_rows): every hit the production
@@ -269,8 +334,8 @@ __device__ __forceinline__ void mm_find_slots(const TabSpin &T, u64 h, u64 key, 
     beg = end = 0;
     u64 pos = h & T.mm_mask;
     while (true) {
-        const ulonglong2 v = __ldg(T.mm + 2 * pos);
-        const ulonglong2 w = __ldg(T.mm + 2 * pos + 1);
+        const ulonglong2 v = ld_stream(T.mm + 2 * pos);
+        const ulonglong2 w = ld_stream(T.mm + 2 * pos + 1);
         const uint32_t sm = (uint32_t)v.y;
         if (sm == MM_EMPTY) return;
         if (v.x == key && sm == meta) {
@@ -289,8 +354,8 @@ __device__ __forceinline__ void mm_find(const TabSpin &T, u64 key, uint32_t meta
     if (!((bw >> ((h >> 20) & 63)) & (bw >> ((h >> 26) & 63)) & 1)) return;
     u64 pos = h & T.mm_mask;
     while (true) {
-        const ulonglong2 v = __ldg(T.mm + 2 * pos);
-        const ulonglong2 w = __ldg(T.mm + 2 * pos + 1);
+        const ulonglong2 v = ld_stream(T.mm + 2 * pos);
+        const ulonglong2 w = ld_stream(T.mm + 2 * pos + 1);
         const uint32_t sm = (uint32_t)v.y;
         if (sm == MM_EMPTY) return;
         if (v.x == key && sm == meta) {
@@ -333,10 +398,11 @@ struct RowState {
 // psi_hat(x) < e^-600 (exp / sincos, large code) is a separate instantiation
 // (DIRECT), so this stays small and no ABI call forces the kernel's live
 // registers to local memory.
-template <bool DIRECT, bool OCC>
+template <bool DIRECT, bool OCC, bool AB, bool LOG>
 __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *psi_hat, const double2 *logpsi,
                                              const int2 *q, int qh, int cnt, const RowState *rs, double2 *acc,
-                                             const double *occ_rec, int nq, const HitLog &lg) {
+                                             const double *occ_rec, int nq, const HitLog &lg, const double *ab_d,
+                                             const ulonglong2 *pair_J, int64_t P) {
     const int lane = threadIdx.x & 31;
     uint32_t c_hit = 0, c_str = 0;
     __syncwarp();
@@ -345,11 +411,12 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
     int2 e = make_int2(-1, 0);
     uint32_t gb0 = 0, ge0 = 0;
     double2 ps0 = make_double2(0.0, 0.0);
-    bool occ = false;
+    bool occ = false, ab = false;
     if (lane < cnt) {
         e = q[(qh + lane) & (QCAP - 1)];          // ring buffer: no shifting after a flush
         occ = OCC && e.x < 0;                      // single excitation, occupation-form record
-        if (!occ) {
+        ab = AB && !occ && !(e.x & REC_TAG) && (e.x & AB_TAG);   // alpha x beta, closed form
+        if (!occ && !ab) {
             if (e.x & REC_TAG) {                   // 1-4 folded strings, start and count carried in the tag
                 gb0 = (uint32_t)(e.x & 0x0FFFFFFF);
                 ge0 = gb0 + 1 + ((e.x >> 28) & 3);
@@ -359,11 +426,14 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
                 ge0 = be.y;
             }
         }
-        if (!direct) ps0 = __ldg(psi_hat + e.y);   // issued with the offsets, used after the sum
+        if (!direct) {                             // issued with the offsets, used after the sum
+            const ulonglong2 pv = ld_keep(reinterpret_cast<const ulonglong2 *>(psi_hat + e.y));
+            ps0 = make_double2(__longlong_as_double((long long)pv.x), __longlong_as_double((long long)pv.y));
+        }
         ++c_hit;
     }
     auto add = [&](double hv, int64_t idx) {
-        if (lg.count) log_hit(lg, rs->row, idx, hv);
+        if (LOG && lg.count) log_hit(lg, rs->row, idx, hv);
         double2 ps = ps0;
         if (direct) {
             const double2 lx = rs->lx;
@@ -395,7 +465,11 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
         add(hv, e.y);
     }
     const bool big = lane < cnt && !occ && ge0 - gb0 > 32;
-    if (lane < cnt && !occ && !big) {
+    if (AB && ab) {
+        add(ab_value(ab_d, pair_J, P, ((uint32_t)e.x >> 11) & 0x7FF, (uint32_t)e.x & 0x7FF, x0, x1), e.y);
+        ++c_str;
+    }
+    if (lane < cnt && !occ && !big && !ab) {
         // 4 strings in flight per lane (loads issued before the sums; same order)
         double hv = 0.0;
         for (uint32_t i0 = gb0; i0 < ge0; i0 += 4) {
@@ -454,6 +528,9 @@ __device__ unsigned long long g_prof[16];
 #define NNQS_PHASE_MASK 15
 #endif
 #define WARPS_PER_BLOCK 8
+#ifndef NNQS_AB
+#define NNQS_AB 1      // alpha x beta groups in closed form (SpinIndex::ab_ok)
+#endif
 #ifndef NNQS_SPIN_MINB
 #define NNQS_SPIN_MINB 4
 #endif
@@ -471,7 +548,7 @@ __device__ unsigned long long g_prof[16];
 // partial2 != NULL: phase (ii) (PH = 20) runs concurrently with PH = 3 on its own
 // stream, starts from zero and writes partial2; PH = 24 starts from
 // partial + partial2 (a row's order is still fixed by the row and the table).
-template <int PH, int MINB, bool DIRECT>
+template <int PH, int MINB, bool DIRECT, bool LOG>
 __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G, TabSpin T, int64_t row_begin,
                                                    int64_t n_rows, double2 *out,
                                                    unsigned long long *stats, unsigned long long pairs,
@@ -563,9 +640,15 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
         __syncwarp();
         int qn = 0, qh = 0;                          // warp-uniform ring length and head
         auto flush = [&](int cnt) {                  // lanes < cnt evaluate q[qh + lane]
+            if (phase_mask & 64) {                   // profiling builds only: hits found, not evaluated
+                qh = (qh + cnt) & (QCAP - 1);
+                qn -= cnt;
+                return;
+            }
             PROF_T(t_fl)
-            const uint2 fo = flush_queue<DIRECT, (PH & 6) != 0>(G, T.psi_hat, T.logpsi, q, qh, cnt, rs, acc, S.occ_rec, S.nq,
-                                                                  T.log);
+            const uint2 fo = flush_queue<DIRECT, (PH & 6) != 0, (PH & 8) != 0, LOG>(G, T.psi_hat, T.logpsi, q, qh, cnt, rs, acc,
+                                                                                S.occ_rec, S.nq, T.log, S.ab_d,
+                                                                                S.pair_J, S.P);
             c_hit += fo.x;
             c_str += fo.y;
             qh = (qh + cnt) & (QCAP - 1);
@@ -661,7 +744,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                 hv = warp_strided_sum(G, gb, ge, rs->x0, rs->x1);
             }
             if (lane == 0) {   // x' = x: psi_hat(x) (or 1 on the direct path)
-                if (T.log.count) log_hit(T.log, (int)i, i, hv);
+                if (LOG && T.log.count) log_hit(T.log, (int)i, i, hv);
                 double2 ps = make_double2(1.0, 0.0);
                 if (!DIRECT) ps = __ldg(T.psi_hat + i);
                 double2 ac = acc[0];
@@ -741,7 +824,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                     int32_t mb = 0, me = 0;
                     if (live) mm_find(T, key, meta, mb, me);
                     drain(mb, me, want, [&](int32_t mj, int32_t swant, int32_t &k, int32_t &idx) {
-                        const ulonglong2 en = __ldg(T.mm_ent + mj);
+                        const ulonglong2 en = ld_stream(T.mm_ent + mj);
                         idx = (int32_t)en.y;
                         const u64 d = mine ^ en.x;
                         if (__popcll(d) == swant) k = same_spin_tag(S, ph, d, swant, s_lut);
@@ -813,13 +896,13 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                     if (lane < np - cnt) pl[lane] = pl[lane + cnt];
                     np -= cnt;
                     drain(mb, me, ur, [&](int32_t mj, int32_t sur, int32_t &k, int32_t &idx) {
-                        const ulonglong2 en = __ldg(T.mm_ent + mj);
+                        const ulonglong2 en = ld_stream(T.mm_ent + mj);
                         idx = (int32_t)en.y;
                         const u64 d = b ^ en.x;
                         if (d) {
                             const int r1 = __ffsll((long long)d) - 1;
                             const int r2 = 63 - __clzll((long long)d);
-                            k = __ldg(S.ab_rec + (int64_t)sur * S.P + pair_rank(r1, r2, S.n));
+                            k = ab_key(S, sur, pair_rank(r1, r2, S.n));
                         }
                     });
                 }
@@ -882,7 +965,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         if (__popcll(d) == 2 && (T.uniform_pc || __popcll(b & d) == 1)) {
                             const int r1 = __ffsll((long long)d) - 1;
                             const int r2 = 63 - __clzll((long long)d);
-                            kk[u] = __ldg(S.ab_rec + (int64_t)ur[u] * S.P + pair_rank(r1, r2, S.n));
+                            kk[u] = ab_key(S, ur[u], pair_rank(r1, r2, S.n));
                             ix[u] = __ldg(T.listA_idx + jj[u]);
                         }
                         c_cand += (f0 + 32 * u + lane) < total;
@@ -1356,6 +1439,7 @@ __global__ void k_hj_bounds(const u64 *keys, int64_t m, int shift, int32_t *kb, 
 }
 
 // one warp per row of the heavy groups: sum its sorted hits (fixed lane order)
+template <bool LOG>
 __global__ void k_hj_eval(SpinView S, GroupView G, TabSpin T, const int32_t *heavy_groups, int n_heavy,
                           int64_t row_begin, int64_t row_end, const u64 *keys, int ibits, int kbits, const int32_t *kb,
                           const int32_t *ke, double2 *acc, unsigned long long *stats) {
@@ -1407,7 +1491,7 @@ __global__ void k_hj_eval(SpinView S, GroupView G, TabSpin T, const int32_t *hea
                             hv += flip_sign2(g_d(G, i), (__popcll(xk.x & Z.x) + __popcll(xk.y & Z.y)) & 1);
                         }
                         c_str += b1[u] - b0[u];
-                        if (T.log.count) log_hit(T.log, e, ix[u], hv);
+                        if (LOG && T.log.count) log_hit(T.log, e, ix[u], hv);
                         ar = fma(hv, ps[u].x, ar);
                         ai = fma(hv, ps[u].y, ai);
                         ++c_hit;
@@ -1427,7 +1511,7 @@ __global__ void k_hj_eval(SpinView S, GroupView G, TabSpin T, const int32_t *hea
                     k = S.ab_k[pair_rank(p1, p2, S.n) * S.P + pair_rank(r1, r2, S.n)];
                 }
                 const double hv = group_value1(G, k, xk.x, xk.y, c_str);
-                if (T.log.count) log_hit(T.log, e, idx, hv);
+                if (LOG && T.log.count) log_hit(T.log, e, idx, hv);
                 double2 ps;
                 if (!direct) {
                     ps = T.psi_hat[idx];
@@ -1736,6 +1820,53 @@ int nnqs_spin_index_build(const HostTable &H, SpinIndex &S) {
         const uint32_t b0 = S.foff[k], b1 = S.foff[k + 1];
         S.ab_rec[i] = (b1 == b0 + 1 && b0 < 0x10000000u && k < 0x40000000) ? (int32_t)(0x40000000u | b0) : k;
     }
+    // ---- alpha x beta groups in closed form (SpinIndex::ab_ok): the folded group is
+    // one string equal to canon(J) (or none: the strings cancelled, value 0); any
+    // other shape leaves the path on the per-string records
+    S.ab_ok = N <= 128 && S.P <= 2048 && K < 0x20000000;
+    if (S.ab_ok) {
+        S.pair_sites.assign(std::max<int64_t>(S.P, 1), 0);
+        for (int p = 0; p < n; ++p)
+            for (int q = p + 1; q < n; ++q) S.pair_sites[pair_rank(p, q, n)] = (uint32_t)p | ((uint32_t)q << 8);
+        S.ab_w = (S.P + 63) / 64;
+        S.ab_d.assign(std::max<int64_t>(S.P * S.P, 1), std::numeric_limits<double>::quiet_NaN());   // NaN: no group
+        S.ab_bits.assign(std::max<int64_t>(S.P * S.ab_w, 1), 0);
+        auto between = [](int lo, int hi, u64 &m0, u64 &m1) {   // qubits lo < j < hi
+            for (int j = lo + 1; j < hi; ++j) (j < 64 ? m0 : m1) ^= 1ULL << (j & 63);
+        };
+        S.pair_J.assign(4 * std::max<int64_t>(S.P, 1), 0);
+        for (int64_t U = 0; U < S.P; ++U) {
+            const int p = S.pair_sites[U] & 0xFF, q = S.pair_sites[U] >> 8;
+            between(2 * p, 2 * q, S.pair_J[2 * U], S.pair_J[2 * U + 1]);
+            between(2 * p + 1, 2 * q + 1, S.pair_J[2 * (S.P + U)], S.pair_J[2 * (S.P + U) + 1]);
+        }
+        for (int64_t U = 0; U < S.P && S.ab_ok; ++U)
+            for (int64_t V = 0; V < S.P; ++V) {
+                const int32_t k = S.ab_k[U * S.P + V];
+                if (k < 0) continue;
+                const int p = S.pair_sites[U] & 0xFF, q = S.pair_sites[U] >> 8;
+                const int r = S.pair_sites[V] & 0xFF, s2 = S.pair_sites[V] >> 8;
+                const int qa = 2 * p, qb = 2 * q, qc = 2 * r + 1, qd = 2 * s2 + 1;
+                u64 Z0 = S.pair_J[2 * U] ^ S.pair_J[2 * (S.P + V)];
+                u64 Z1 = S.pair_J[2 * U + 1] ^ S.pair_J[2 * (S.P + V) + 1];
+                double sign = 1.0;
+                for (int g2 = 0; g2 < 2; ++g2) {           // canonical representative: clear the low site
+                    const int lo = g2 == 0 ? qa : qc, hi = g2 == 0 ? qb : qd;
+                    if (((lo < 64 ? Z0 : Z1) >> (lo & 63)) & 1) {
+                        (lo < 64 ? Z0 : Z1) ^= 1ULL << (lo & 63);
+                        (hi < 64 ? Z0 : Z1) ^= 1ULL << (hi & 63);
+                        sign = -sign;                      // popc(x & pair) is odd in sector
+                    }
+                }
+                const uint32_t b0 = S.foff[k], b1 = S.foff[k + 1];
+                double v = 0.0;
+                if (b1 == b0 + 1 && S.fz[2 * b0] == Z0 && S.fz[2 * b0 + 1] == Z1) v = sign * S.fd[b0];
+                else if (b1 != b0) { S.ab_ok = false; break; }
+                S.ab_d[U * S.P + V] = v;
+                S.ab_bits[U * S.ab_w + (V >> 6)] |= 1ULL << (V & 63);
+            }
+        if (!S.ab_ok) { S.ab_d.clear(); S.ab_bits.clear(); S.pair_sites.clear(); S.pair_J.clear(); }
+    }
     // ---- same-spin quads likewise (their folded groups hold up to 3 strings)
     for (int sp = 0; sp < 2; ++sp) {
         S.quad_rec[sp].assign(S.quad_k[sp].size(), -1);
@@ -1851,6 +1982,18 @@ int nnqs_spin_index_upload(nnqs_ham h) {
         if ((rc = cuda_check(cudaMemcpy(D.ab_rec, S.ab_rec.data(), bab, cudaMemcpyHostToDevice), "copy ab_rec"))) return rc;
         D.bytes += (int64_t)bab;
     }
+    if (S.ab_ok) {
+        const size_t bd = 8 * S.ab_d.size(), bb = 8 * S.ab_bits.size();
+        const size_t bj = 8 * S.pair_J.size();
+        if ((rc = cuda_check(cudaMalloc((void **)&D.pair_J, bj), "alloc pair_J"))) return rc;
+        if ((rc = cuda_check(cudaMemcpy(D.pair_J, S.pair_J.data(), bj, cudaMemcpyHostToDevice), "copy pair_J"))) return rc;
+        D.bytes += (int64_t)bj;
+        if ((rc = cuda_check(cudaMalloc((void **)&D.ab_d, bd), "alloc ab_d"))) return rc;
+        if ((rc = cuda_check(cudaMalloc((void **)&D.ab_bits, bb), "alloc ab_bits"))) return rc;
+        if ((rc = cuda_check(cudaMemcpy(D.ab_d, S.ab_d.data(), bd, cudaMemcpyHostToDevice), "copy ab_d"))) return rc;
+        if ((rc = cuda_check(cudaMemcpy(D.ab_bits, S.ab_bits.data(), bb, cudaMemcpyHostToDevice), "copy ab_bits"))) return rc;
+        D.bytes += (int64_t)(bd + bb);
+    }
     if (S.occ_ok) {
         const size_t bo2 = 8 * S.occ_rec.size();
         if ((rc = cuda_check(cudaMalloc((void **)&D.occ_rec, bo2), "alloc occ"))) return rc;
@@ -1898,6 +2041,12 @@ void nnqs_spin_index_release(nnqs_ham h) {
     D.ab_k = nullptr;
     cudaFree(D.ab_rec);
     D.ab_rec = nullptr;
+    cudaFree(D.ab_d);
+    cudaFree(D.ab_bits);
+    cudaFree(D.pair_J);
+    D.pair_J = nullptr;
+    D.ab_d = nullptr;
+    D.ab_bits = nullptr;
     cudaFree(D.diag_uv);
     D.diag_uv = nullptr;
     cudaFree(D.occ_rec);
@@ -2344,7 +2493,8 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
     SpinView sv{S.n, S.P, D.pair_k[0], D.pair_k[1], D.quad_k[0], D.quad_k[1], D.ab_k, D.ab_rec ? D.ab_rec : D.ab_k,
                 D.quad_rec[0] ? D.quad_rec[0] : D.quad_k[0], D.quad_rec[1] ? D.quad_rec[1] : D.quad_k[1],
                 S.diag_k,
-                h->host.n_qubits, S.occ_ok ? D.occ_rec : nullptr, S.diag_K, S.diag_ok ? D.diag_uv : nullptr};
+                h->host.n_qubits, S.occ_ok ? D.occ_rec : nullptr, S.diag_K, S.diag_ok ? D.diag_uv : nullptr,
+                (S.ab_ok && NNQS_AB) ? D.ab_d : nullptr, D.ab_bits, S.ab_w, (const ulonglong2 *)D.pair_J};
     GroupView gv{(const uint2 *)D.frng, (const ulonglong2 *)D.frec};   // in-sector folded strings
     TabSpin tv{t->n, (const ulonglong2 *)t->keys, (const double2 *)t->logpsi, (const double2 *)t->psi_hat,
                t->slots, t->bucket_mask, t->shift_key, t->sa, t->sb, t->ga_of, t->gb_of, t->offA, t->offB,
@@ -2422,9 +2572,9 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
             cub::DeviceRadixSort::SortPairsDescending(tmp, tb1, cs3[k], ks, io, ps[k], (int)n_rows, 0, 32, st);
         }
     }
-    rc = cuda_check(nnqs_malloc_async((void **)&ctr, 64, st), "alloc row counters");
+    rc = cuda_check(nnqs_malloc_async((void **)&ctr, 128, st), "alloc row counters");
     if (rc) return cleanup(rc);
-    cudaMemsetAsync(ctr, 0, 64, st);
+    cudaMemsetAsync(ctr, 0, 128, st);   // [0, 6): the row kernels' row counters
     rc = cuda_check(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming), "event");
     if (!rc) rc = cuda_check(cudaEventCreateWithFlags(&ev_hj, cudaEventDisableTiming), "event");
     if (!rc) rc = cuda_check(cudaEventCreateWithFlags(&ev_p2, cudaEventDisableTiming), "event");
@@ -2444,11 +2594,24 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
     // three launches, each a smaller kernel (instruction cache): diagonal + phase (i)
     // -> partial; phase (ii) (s2, concurrent) -> partial2; phase (iii) starts from
     // partial + partial2 and finalises (fused chunk partials of Eq. (6) included)
-    launch(k_eloc_spin<3, 4, false>, perm3, st);
-    launch(k_eloc_spin<20, 4, false>, perm20, s2);
+    // the parity hit log (nnqs_coupled_debug_rows) has instantiations of its own, so
+    // the production kernels carry none of its code
+    const bool lg_on = lg.count != nullptr;
+    if (lg_on) {
+        launch(k_eloc_spin<3, 4, false, true>, perm3, st);
+        launch(k_eloc_spin<20, 4, false, true>, perm20, s2);
+    } else {
+        launch(k_eloc_spin<3, 4, false, false>, perm3, st);
+        launch(k_eloc_spin<20, 4, false, false>, perm20, s2);
+    }
     if (t->n_direct) {
-        launch(k_eloc_spin<3, 4, true>, perm3, st);
-        launch(k_eloc_spin<20, 4, true>, perm20, s2);
+        if (lg_on) {
+            launch(k_eloc_spin<3, 4, true, true>, perm3, st);
+            launch(k_eloc_spin<20, 4, true, true>, perm20, s2);
+        } else {
+            launch(k_eloc_spin<3, 4, true, false>, perm3, st);
+            launch(k_eloc_spin<20, 4, true, false>, perm20, s2);
+        }
     }
     cudaEventRecord(ev_p2, s2);
     cudaStreamWaitEvent(st, ev_p2, 0);
@@ -2495,17 +2658,25 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
                                                kbits + ibits + rbits, hs);
                 cub::DeviceRadixSort::SortKeys(htmp, tb, hkeys, k2, (int)m, kbits, kbits + ibits + rbits, hs);
                 k_hj_bounds<<<grid_for((int64_t)m, 256), 256, 0, hs>>>(k2, (int64_t)m, ibits + kbits, kb, ke);
-                k_hj_eval<<<148 * hj_ev, 256, 0, hs>>>(sv, gv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end, k2,
+                auto hj_eval = lg_on ? k_hj_eval<true> : k_hj_eval<false>;
+                hj_eval<<<148 * hj_ev, 256, 0, hs>>>(sv, gv, tv, t->heavy_groups, t->n_heavy, row_begin, row_end, k2,
                                                    ibits, kbits, kb, ke, acc_heavy, (unsigned long long *)stats);
             }
             break;
         }
+    }
+    if (do_hj) {
         cudaEventRecord(ev_hj, hs);
         cudaStreamWaitEvent(st, ev_hj, 0);
     }
     if (!rc) {
-        launch(k_eloc_spin<24, 4, false>, perm24, st);
-        if (t->n_direct) launch(k_eloc_spin<24, 4, true>, perm24, st);
+        if (lg_on) {
+            launch(k_eloc_spin<24, 4, false, true>, perm24, st);
+            if (t->n_direct) launch(k_eloc_spin<24, 4, true, true>, perm24, st);
+        } else {
+            launch(k_eloc_spin<24, 4, false, false>, perm24, st);
+            if (t->n_direct) launch(k_eloc_spin<24, 4, true, false>, perm24, st);
+        }
     }
     return cleanup(rc);
 }
