@@ -309,6 +309,33 @@ int nnqs_coupled_debug_rows(nnqs_ham h, nnqs_table t, int64_t row_begin, int64_t
                             int64_t *row_id, int64_t *group_id, uint64_t *xprime, int64_t *table_idx,
                             double *h_xxp, int64_t *n_pairs_out);
 
+/*
+ * nnqs_bas_layer -- one local sampling step of batch autoregressive sampling
+ * (BAS, Fig. 3(b); stage 1 of the data-centric iteration).
+ * Input: the m unique prefixes of the current layer (device keys u64[m][2] in
+ * the sample-key layout: qubit 2p = spin-up orbital p, 2p+1 = spin-down; only
+ * orbitals > `orbital` set), their weights (device i64[m], >= 0) and the model's
+ * conditional distribution over the next two qubits (device f64[m][4], outcome
+ * o: up bit o & 1, down bit o >> 1; unnormalised values are fine).  Orbitals are
+ * sampled from n_orbitals - 1 down to 0 (the reverse qubit order).
+ * Each prefix's weight w is split among its 4 children by a multinomial draw of
+ * exactly w samples from the masked, renormalised distribution (Eq. 12, P:290:
+ * outcomes exceeding n_up / n_dn are zeroed; so are outcomes that can no longer
+ * reach them -- DESIGN.md R24), as a chain of conditional binomials with
+ * uniforms from a counter-based generator keyed by (seed, orbital, prefix key):
+ * a node's children depend on the node alone, so any split of a layer over
+ * ranks (parallel BAS) reproduces the serial result exactly.
+ * Output: the children with weight > 0 (zero-weight leaves pruned),
+ * device keys_out u64[4m][2] / counts_out i64[4m] (capacity 4m), in (parent,
+ * outcome) order -- ascending keys when the input is ascending; *m_out (host)
+ * = how many.  Synchronises cuda_stream.  Errors: NNQS_E_ARG (bad pointers, or
+ * a prefix with weight > 0 and no feasible outcome), NNQS_E_SIZE (orbital
+ * outside [0, n_orbitals), n_orbitals > 64, m >= 2^29), NNQS_E_NOMEM/_CUDA.
+ */
+int nnqs_bas_layer(const uint64_t *keys, const int64_t *counts, const double *probs, int64_t m, int orbital,
+                   int n_orbitals, int n_up, int n_dn, uint64_t seed, uint64_t *keys_out, int64_t *counts_out,
+                   int64_t *m_out, void *cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

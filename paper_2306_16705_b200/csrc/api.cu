@@ -94,6 +94,7 @@ int finish_ham(nnqs_ham h, int device, nnqs_ham *out) {
     int rc = nnqs_ham_upload(h);
     if (!rc) rc = nnqs_spin_index_upload(h);
     if (rc) {
+        nnqs_spin_index_release(h);
         nnqs_ham_release(h);
         delete h;
         return rc;
@@ -204,8 +205,8 @@ int nnqs_ham_free(nnqs_ham h) {
     if (!h) return NNQS_OK;
     if (h->device >= 0) {
         DeviceGuard g(h->device);
+        nnqs_spin_index_release(h);     // before nnqs_ham_release resets the DeviceHam
         nnqs_ham_release(h);
-        nnqs_spin_index_release(h);
     }
     delete h;
     return NNQS_OK;

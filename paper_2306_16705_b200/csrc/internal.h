@@ -101,6 +101,7 @@ struct DeviceHam {
     // term arrays [Nh]
     void *tz = nullptr;       // ulonglong2 Z mask
     double *td = nullptr;     // fused coefficient d
+    void *glit = nullptr;     // [K] 32-B {X, h(X), info} records of the literal kernel
     // spin index (structured path)
     int32_t *pair_k[2] = {nullptr, nullptr};
     int32_t *quad_k[2] = {nullptr, nullptr};

@@ -284,6 +284,194 @@ __global__ void __launch_bounds__(256) k_eloc_v1(HamView H, TabView T, int64_t r
     }
 }
 
+// ------------------------------------------ literal Algorithm 2, staged (v2)
+// The same loop as k_eloc_v1 (every row x every group, ascending k; sector
+// test, lookup, string sum on a hit) with the group table
+// streamed through shared memory: 32-B records {X, h(X), sector info} in tiles of
+// LIT_TILE groups, fetched by the bulk-copy engine (cp.async.bulk + mbarrier,
+// LIT_STAGES deep) while the CTA works on the previous tiles, each tile read by
+// the LIT_THREADS rows of the CTA (one row per thread; one tile load per 1024
+// rows instead of one broadcast load per warp and group).  Hits are applied in
+// ascending k, so a row's sum is bit-identical to k_eloc_v1's.
+#define LIT_THREADS 512
+#define LIT_TILE 1024
+#define LIT_STAGES 4
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n LAB_WAIT:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra LAB_WAIT;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+struct LitRec {
+    ulonglong2 x;      // flip mask X_k
+    u64 hx;            // h(X_k)
+    uint32_t info;     // popc(X & alpha) / 2 | popc(X & beta) / 2 << 8 | odd << 16
+    uint32_t pad;
+};
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int MODE, bool CONS>
+__global__ void __launch_bounds__(LIT_THREADS, 1) k_eloc_lit(HamView H, const LitRec *rec, TabView T,
+                                                             int64_t row_begin, const ulonglong2 *rows,
+                                                             const double2 *row_lp, int64_t n_rows, double2 *out,
+                                                             unsigned long long *stats, ChunkSink cs) {
+    extern __shared__ __align__(128) unsigned char lit_smem[];
+    LitRec *tile = reinterpret_cast<LitRec *>(lit_smem);                    // [LIT_STAGES][LIT_TILE]
+    __shared__ __align__(8) unsigned long long full[LIT_STAGES], empty[LIT_STAGES];
+    constexpr int kWarps = LIT_THREADS / 32;
+    const double s = dkey_inv(*T.shift_key);
+    const int64_t K = H.K;
+    const int64_t n_tiles = (K + LIT_TILE - 1) / LIT_TILE;
+    const int lane = threadIdx.x & 31;
+    u64 c_pairs = 0, c_sec = 0, c_hit = 0, c_str = 0;
+    // every row block of this CTA streams the whole table: one continuous ring of
+    // tiles (global tile counter q = block * n_tiles + t, stage q % S, phase q / S)
+    const int64_t stride = (int64_t)gridDim.x * LIT_THREADS;
+    const int64_t first = (int64_t)blockIdx.x * LIT_THREADS;
+    const int64_t n_blocks = first < n_rows ? (n_rows - first + stride - 1) / stride : 0;
+    const int64_t q_end = n_blocks * n_tiles;
+    auto issue = [&](int64_t q) {                 // producer: tile q % n_tiles into stage q % S
+        const int st = (int)(q % LIT_STAGES);
+        const int64_t g0 = (q % n_tiles) * LIT_TILE;
+        const unsigned bytes = (unsigned)(min((int64_t)LIT_TILE, K - g0) * (int64_t)sizeof(LitRec));
+        mbar_expect_tx(&full[st], bytes);
+        bulk_g2s(tile + st * LIT_TILE, rec + g0, bytes, &full[st]);
+    };
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < LIT_STAGES; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], kWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int64_t q = 0; q < LIT_STAGES && q < q_end; ++q) issue(q);
+    int64_t q = 0;
+    for (int64_t blk = 0; blk < n_blocks; ++blk) {
+        const int64_t r = first + blk * stride + threadIdx.x;
+        u64 x0 = 0, x1 = 0;
+        double2 lx = make_double2(-INFINITY, 0.0);
+        if (r < n_rows) {
+            if (rows) {
+                const ulonglong2 k = rows[r];
+                x0 = k.x;
+                x1 = k.y;
+                lx = row_lp[r];
+            } else {
+                const int64_t i = row_begin + r;
+                if (MODE == 0) {
+                    const ulonglong2 k = T.keys[i];
+                    x0 = k.x;
+                    x1 = k.y;
+                } else {
+                    x0 = (u64)i;
+                }
+                lx = T.logpsi[i];
+            }
+        }
+        const bool live = lx.x > -INFINITY;      // psi(x) = 0 (reading R10) or past the end: no pairs
+        const bool direct = (lx.x - s) < -600.0;
+        const u64 hx = (MODE == 0 && live) ? hash128(x0, x1) : 0;
+        double ar = 0.0, ai = 0.0;
+        for (int64_t t = 0; t < n_tiles; ++t, ++q) {
+            const int st = (int)(q % LIT_STAGES);
+            const unsigned ph = (unsigned)((q / LIT_STAGES) & 1);
+            mbar_wait(&full[st], ph);
+            const LitRec *tl = tile + st * LIT_TILE;
+            const int gn = live ? (int)min((int64_t)LIT_TILE, K - t * LIT_TILE) : 0;
+            for (int g = 0; g < gn; ++g) {
+                const LitRec R = tl[g];
+                if (CONS) {
+                    const int na = __popcll(x0 & R.x.x & ALPHA_MASK) + __popcll(x1 & R.x.y & ALPHA_MASK);
+                    const int nb = __popcll(x0 & R.x.x & BETA_MASK) + __popcll(x1 & R.x.y & BETA_MASK);
+                    if (na != (int)(R.info & 0xff) || nb != (int)((R.info >> 8) & 0xff)) continue;
+                }
+                ++c_sec;
+                const u64 p0 = x0 ^ R.x.x, p1 = x1 ^ R.x.y;
+                int64_t idx;
+                if (MODE == 1) idx = (p1 == 0 && p0 < (u64)T.n) ? (int64_t)p0 : -1;
+                else idx = probe(T, hx ^ R.hx, p0, p1);
+                if (idx < 0) continue;
+                ++c_hit;
+                const double hv = group_value(H, t * LIT_TILE + g, x0, x1, c_str);
+                double2 ps;
+                if (!direct) {
+                    ps = __ldg(T.psi_hat + idx);
+                } else {
+                    const double2 l = T.logpsi[idx];
+                    const double m = exp(l.x - lx.x);
+                    double sn, cs2;
+                    sincos(l.y - lx.y, &sn, &cs2);
+                    ps = make_double2(m * cs2, m * sn);
+                }
+                ar = fma(hv, ps.x, ar);
+                ai = fma(hv, ps.y, ai);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);   // this warp is done with stage st
+            if (threadIdx.x == 0 && q + LIT_STAGES < q_end) {
+                mbar_wait(&empty[st], ph);            // every warp released it
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(q + LIT_STAGES);
+            }
+        }
+        if (r < n_rows) {
+            double2 e;
+            if (!live) {
+                e = make_double2(NAN, NAN);
+            } else if (direct) {
+                e = make_double2(ar, ai);
+            } else {
+                // E = acc / psi_hat(x) = acc * exp(-(logpsi(x) - s))
+                const double m = exp(-(lx.x - s));
+                double sn, cs2;
+                sincos(-lx.y, &sn, &cs2);
+                const double ir = m * cs2, ii = m * sn;
+                e = make_double2(ar * ir - ai * ii, ar * ii + ai * ir);
+            }
+            if (live) c_pairs += (u64)K;
+            out[r] = e;
+            chunk_done_thread(cs, out, r, n_rows);
+        }
+    }
+    if (stats) {
+        for (int o = 16; o; o >>= 1) {
+            c_pairs += __shfl_xor_sync(0xffffffffu, c_pairs, o);
+            c_sec += __shfl_xor_sync(0xffffffffu, c_sec, o);
+            c_hit += __shfl_xor_sync(0xffffffffu, c_hit, o);
+            c_str += __shfl_xor_sync(0xffffffffu, c_str, o);
+        }
+        if (lane == 0) {
+            atomicAdd(stats + 0, c_pairs);
+            atomicAdd(stats + 1, c_sec);
+            atomicAdd(stats + 2, c_hit);
+            atomicAdd(stats + 3, c_str);
+        }
+    }
+}
+
 template <int MODE, bool CONS>
 __global__ void k_coupled_debug(HamView H, TabView T, const ulonglong2 *rows, int64_t n_rows,
                                 int64_t max_pairs, int64_t *oi, u64 *ox, double *oh,
@@ -408,13 +596,20 @@ int nnqs_ham_upload(nnqs_ham h) {
         if ((rc = cuda_check(cudaMemcpy(D.tz, H.z.data(), bz, cudaMemcpyHostToDevice), "copy tz"))) return rc;
         if ((rc = cuda_check(cudaMemcpy(D.td, H.d.data(), bd, cudaMemcpyHostToDevice), "copy td"))) return rc;
     }
-    D.bytes = (int64_t)(bx + bh + bi + bo + bz + bd);
+    // the literal kernel's 32-B group records {X, h(X), info} (k_eloc_lit streams them)
+    std::vector<LitRec> lit(std::max<int64_t>(K, 1));
+    for (int64_t k = 0; k < K; ++k) lit[k] = LitRec{make_ulonglong2(H.x[2 * k], H.x[2 * k + 1]), hx[k], info[k], 0};
+    const size_t bl = sizeof(LitRec) * lit.size();
+    if ((rc = cuda_check(cudaMalloc(&D.glit, bl), "cudaMalloc glit"))) return rc;
+    if ((rc = cuda_check(cudaMemcpy(D.glit, lit.data(), bl, cudaMemcpyHostToDevice), "copy glit"))) return rc;
+    D.bytes = (int64_t)(bx + bh + bi + bo + bz + bd + bl);
     return NNQS_OK;
 }
 
 void nnqs_ham_release(nnqs_ham h) {
     DeviceHam &D = h->dev;
     cudaFree(D.gx); cudaFree(D.ghx); cudaFree(D.ginfo); cudaFree(D.goff); cudaFree(D.tz); cudaFree(D.td);
+    cudaFree(D.glit);
     D = DeviceHam();
 }
 
@@ -488,6 +683,19 @@ int nnqs_launch_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const 
     auto *rl = (const double2 *)row_logpsi;
     auto *o = (double2 *)eloc;
     auto *s = (unsigned long long *)stats;
+#ifndef NNQS_LIT_V1
+#define NNQS_LIT_V1 0                             // A/B builds only: the unstaged k_eloc_v1
+#endif
+    if (h->dev.glit && !NNQS_LIT_V1) {            // staged literal kernel (k_eloc_lit)
+        auto kern = t->mode == 0 ? (cons ? k_eloc_lit<0, true> : k_eloc_lit<0, false>)
+                                 : (cons ? k_eloc_lit<1, true> : k_eloc_lit<1, false>);
+        const size_t smem = (size_t)LIT_STAGES * LIT_TILE * sizeof(LitRec);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int64_t blocks = (n_rows + LIT_THREADS - 1) / LIT_THREADS;
+        const int gl = (int)std::min<int64_t>(blocks, 148);
+        kern<<<gl, LIT_THREADS, smem, st>>>(H, (const LitRec *)h->dev.glit, T, row_begin, r, rl, n_rows, o, s, cs);
+        return cuda_check(cudaGetLastError(), "local energy launch");
+    }
     if (t->mode == 0) {
         if (cons) k_eloc_v1<0, true><<<g, 256, 0, st>>>(H, T, row_begin, r, rl, n_rows, o, s, cs);
         else k_eloc_v1<0, false><<<g, 256, 0, st>>>(H, T, row_begin, r, rl, n_rows, o, s, cs);

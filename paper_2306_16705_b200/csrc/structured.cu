@@ -79,43 +79,6 @@ __host__ __device__ __forceinline__ u64 mix64(u64 z) {
 }
 
 
-// L2 eviction-priority hints (PTX createpolicy + ld.global.nc.L2::cache_hint):
-// the multimap's slots and records are touched once per probe and spread over
-// GBs -- marked evict-first so that they do not push the small, reused tables
-// (Bloom words, psi_hat, string lists, folded strings) out of the 126-MB L2.
-#ifndef NNQS_L2HINT
-#define NNQS_L2HINT 0
-#endif
-__device__ __forceinline__ u64 pol_stream() {
-    u64 p;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ u64 pol_keep() {
-    u64 p;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ ulonglong2 ld_hint(const ulonglong2 *ptr, u64 pol) {
-    ulonglong2 v;
-    asm("ld.global.nc.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;" : "=l"(v.x), "=l"(v.y) : "l"(ptr), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ ulonglong2 ld_stream(const ulonglong2 *ptr) {
-#if NNQS_L2HINT & 1
-    return ld_hint(ptr, pol_stream());
-#else
-    return __ldg(ptr);
-#endif
-}
-__device__ __forceinline__ ulonglong2 ld_keep(const ulonglong2 *ptr) {
-#if NNQS_L2HINT & 2
-    return ld_hint(ptr, pol_keep());
-#else
-    return __ldg(ptr);
-#endif
-}
-
 // ------------------------------------------------------------- device views
 struct SpinView {
     int n;
@@ -162,9 +125,9 @@ struct GroupView {
     const ulonglong2 *rec;
 };
 __device__ __forceinline__ uint2 g_range(const GroupView &G, int32_t k) { return __ldg(G.grng + k); }
-__device__ __forceinline__ ulonglong2 g_z(const GroupView &G, uint32_t i) { return ld_keep(G.rec + 2 * i); }
+__device__ __forceinline__ ulonglong2 g_z(const GroupView &G, uint32_t i) { return __ldg(G.rec + 2 * i); }
 __device__ __forceinline__ double g_d(const GroupView &G, uint32_t i) {
-    return __longlong_as_double((long long)ld_keep(G.rec + 2 * i + 1).x);
+    return __longlong_as_double((long long)__ldg(G.rec + 2 * i + 1).x);
 }
 
 // Parity/debug hit log (nnqs_coupled_debug_rows): every hit the production
@@ -334,8 +297,8 @@ __device__ __forceinline__ void mm_find_slots(const TabSpin &T, u64 h, u64 key, 
     beg = end = 0;
     u64 pos = h & T.mm_mask;
     while (true) {
-        const ulonglong2 v = ld_stream(T.mm + 2 * pos);
-        const ulonglong2 w = ld_stream(T.mm + 2 * pos + 1);
+        const ulonglong2 v = __ldg(T.mm + 2 * pos);
+        const ulonglong2 w = __ldg(T.mm + 2 * pos + 1);
         const uint32_t sm = (uint32_t)v.y;
         if (sm == MM_EMPTY) return;
         if (v.x == key && sm == meta) {
@@ -354,8 +317,8 @@ __device__ __forceinline__ void mm_find(const TabSpin &T, u64 key, uint32_t meta
     if (!((bw >> ((h >> 20) & 63)) & (bw >> ((h >> 26) & 63)) & 1)) return;
     u64 pos = h & T.mm_mask;
     while (true) {
-        const ulonglong2 v = ld_stream(T.mm + 2 * pos);
-        const ulonglong2 w = ld_stream(T.mm + 2 * pos + 1);
+        const ulonglong2 v = __ldg(T.mm + 2 * pos);
+        const ulonglong2 w = __ldg(T.mm + 2 * pos + 1);
         const uint32_t sm = (uint32_t)v.y;
         if (sm == MM_EMPTY) return;
         if (v.x == key && sm == meta) {
@@ -426,10 +389,7 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
                 ge0 = be.y;
             }
         }
-        if (!direct) {                             // issued with the offsets, used after the sum
-            const ulonglong2 pv = ld_keep(reinterpret_cast<const ulonglong2 *>(psi_hat + e.y));
-            ps0 = make_double2(__longlong_as_double((long long)pv.x), __longlong_as_double((long long)pv.y));
-        }
+        if (!direct) ps0 = __ldg(psi_hat + e.y);   // issued with the offsets, used after the sum
         ++c_hit;
     }
     auto add = [&](double hv, int64_t idx) {
@@ -458,7 +418,19 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
         for (int hw = 0; hw < 4; ++hw) {           // 32-bit halves: one FLO per occupied qubit
             uint32_t w = (uint32_t)((hw < 2 ? x0 : x1) >> (32 * (hw & 1)));
             const double *rb = rr + 4 + 32 * hw;
-            for (; w; w &= w - 1) sum += __ldg(rb + (__ffs(w) - 1));
+            while (w) {                            // 4 loads in flight, added in ascending R as before
+                double v[4];
+                bool has[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    has[u] = w != 0;
+                    v[u] = has[u] ? __ldg(rb + (__ffs(w) - 1)) : 0.0;
+                    w &= w - 1;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (has[u]) sum += v[u];
+            }
         }
         const double hv = flip_sign2(fma(-2.0, sum, Tg), (__popcll(x0 & B0) + __popcll(x1 & B1)) & 1);
         c_str += __popcll(x0) + __popcll(x1) + 1;
@@ -729,7 +701,16 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                     const int p = oq[l];
                     const double *vp = S.diag_uv + S.nq + (size_t)p * S.nq;
                     double t = __ldg(S.diag_uv + p);
-                    for (int m = l + 1; m < nocc; ++m) t += __ldg(vp + oq[m]);
+                    int m = l + 1;
+                    for (; m + 3 < nocc; m += 4) {       // 4 loads in flight, same order of additions
+                        const double v0 = __ldg(vp + oq[m]), v1 = __ldg(vp + oq[m + 1]);
+                        const double v2 = __ldg(vp + oq[m + 2]), v3 = __ldg(vp + oq[m + 3]);
+                        t += v0;
+                        t += v1;
+                        t += v2;
+                        t += v3;
+                    }
+                    for (; m < nocc; ++m) t += __ldg(vp + oq[m]);
                     hv += t;
                 }
                 for (int o = 16; o; o >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, o);
@@ -824,7 +805,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                     int32_t mb = 0, me = 0;
                     if (live) mm_find(T, key, meta, mb, me);
                     drain(mb, me, want, [&](int32_t mj, int32_t swant, int32_t &k, int32_t &idx) {
-                        const ulonglong2 en = ld_stream(T.mm_ent + mj);
+                        const ulonglong2 en = __ldg(T.mm_ent + mj);
                         idx = (int32_t)en.y;
                         const u64 d = mine ^ en.x;
                         if (__popcll(d) == swant) k = same_spin_tag(S, ph, d, swant, s_lut);
@@ -896,7 +877,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                     if (lane < np - cnt) pl[lane] = pl[lane + cnt];
                     np -= cnt;
                     drain(mb, me, ur, [&](int32_t mj, int32_t sur, int32_t &k, int32_t &idx) {
-                        const ulonglong2 en = ld_stream(T.mm_ent + mj);
+                        const ulonglong2 en = __ldg(T.mm_ent + mj);
                         idx = (int32_t)en.y;
                         const u64 d = b ^ en.x;
                         if (d) {

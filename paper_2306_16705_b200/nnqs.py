@@ -46,6 +46,8 @@ _sig = {
     "nnqs_energy_reduce": ([P, P, I64, P, P], ctypes.c_int),
     "nnqs_coupled_debug": ([P, P, P, I64, I64, P, P, P, P, P, P], ctypes.c_int),
     "nnqs_coupled_debug_rows": ([P, P, I64, I64, I64, P, P, P, P, P, P], ctypes.c_int),
+    "nnqs_bas_layer": ([P, P, P, I64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, P, P,
+                        P, P], ctypes.c_int),
 }
 class Options(ctypes.Structure):
     """nnqs_options (include/nnqs.h): per-table algorithm and list thresholds."""
@@ -297,6 +299,22 @@ def nnqs_grad_weights(eloc, counts, energy_dev, ab_out=None, stream=None):
     _check(_lib.nnqs_grad_weights(_dev_ptr(eloc), _dev_ptr(counts), n, _dev_ptr(energy_dev), _dev_ptr(ab_out),
                                   _stream(stream)))
     return ab_out
+
+
+def nnqs_bas_layer(keys, counts, probs, orbital: int, n_orbitals: int, n_up: int, n_dn: int, seed: int,
+                   stream=None):
+    """One BAS layer (include/nnqs.h): keys CUDA int64 [m, 2], counts CUDA int64 [m],
+    probs CUDA float64 [m, 4] -> (child keys [m', 2], child counts [m']) on the same device."""
+    import torch
+    m = int(keys.shape[0])
+    dev = keys.device
+    ko = torch.empty((max(4 * m, 1), 2), dtype=torch.int64, device=dev)
+    co = torch.empty(max(4 * m, 1), dtype=torch.int64, device=dev)
+    mo = ctypes.c_int64(0)
+    _check(_lib.nnqs_bas_layer(_dev_ptr(keys), _dev_ptr(counts), _dev_ptr(probs), m, int(orbital), int(n_orbitals),
+                               int(n_up), int(n_dn), ctypes.c_uint64(int(seed) & (2**64 - 1)), _dev_ptr(ko),
+                               _dev_ptr(co), ctypes.byref(mo), _stream(stream)))
+    return ko[: mo.value], co[: mo.value]
 
 
 def nnqs_energy_reduce(eloc, counts, stream=None):

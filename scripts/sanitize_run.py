@@ -52,11 +52,26 @@ def run(c, n_rows=None, variant="full", **opt):
     print(f"C{c}/{variant} rows={n} ok", flush=True)
 
 
+def run_bas():
+    """BAS layers (csrc/bas.cu) on a synthetic 20-orbital model, weights up to 10^12."""
+    import numpy as np
+    dev = torch.device("cuda", 0)
+    keys = torch.zeros((1, 2), dtype=torch.int64, device=dev)
+    counts = torch.full((1,), 10**12, dtype=torch.int64, device=dev)
+    rng = np.random.default_rng(3)
+    for orbital in range(19, -1, -1):
+        probs = torch.from_numpy(rng.random((keys.shape[0], 4)) + 0.01).to(dev)
+        keys, counts = nnqs.nnqs_bas_layer(keys, counts, probs, orbital, 20, 7, 7, 11)
+    torch.cuda.synchronize()
+    print(f"BAS 20 orbitals: {keys.shape[0]} unique samples ok", flush=True)
+
+
 if __name__ == "__main__":
     run(2, variant="half")
     run(3)
     run(4)
     run(4, thr_single=3, thr_double=6, thr_rowheavy=40)   # multimap, probes and the join on C4
+    run_bas()
     if "--c5" in sys.argv:
         run(5, n_rows=4096)
     print("sanitize workload done")
