@@ -569,8 +569,10 @@ def run_ours(args):
                    "W": float(energy[3])},
         "stats": {"row_group_pairs": int(st_local[0]), "in_sector_pairs": int(st_local[1]),
                   "hits": int(st_local[2]), "strings_evaluated": int(st_local[3]),
-                  "note": "structured path: in_sector_pairs = candidates examined (list entries, probes), "
-                          "strings_evaluated = folded terms (DESIGN.md R21/R22)"},
+                  "note": "structured path: row_group_pairs = R x K' by definition (the pairs Algorithm 2's "
+                          "loop resolves; the structured kernels resolve them without visiting them, so this "
+                          "is not a counted number), in_sector_pairs = candidates examined (list entries, "
+                          "probes), strings_evaluated = folded terms (DESIGN.md R21-R23)"},
         "rates_per_s": {  # per second of the local-energy call
             "coupled_terms": int(st_local[0]) / max(world, 1) / (kern_avg_ms / 1e3),
             "candidates_examined": int(st_local[1]) / max(world, 1) / (kern_avg_ms / 1e3),

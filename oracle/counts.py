@@ -62,6 +62,34 @@ def group_counts_fast(irreps):
     return 1 + w2 + q_ss + q_os, (1 + N + comb(N, 2)) + 2 * (N - 1) * w2 + 6 * q_ss + 4 * q_os
 
 
+def flip_masks(irreps):
+    """The set of flip masks X (as 128-bit ints) of the JW-mapped Eq. (9) with every
+    symmetry-allowed integral non-zero, written out from the excitation classes
+    (spin orbital (p, sigma) -> qubit 2p + sigma): X = 0; a same-spin pair (p, q) with
+    G_p = G_q (one-body h_pq and the two-body terms with one index pair equal); a
+    same-spin quad with G_p^G_q^G_r^G_s = 0; an up pair x a down pair with equal pair
+    irreps.  Enumeration, no shortcuts: the P1 reference at N = 20 and 120."""
+    g = list(irreps)
+    n = len(g)
+    out = {0}
+    for s in (0, 1):
+        for p, q in itertools.combinations(range(n), 2):
+            if g[p] == g[q]:
+                out.add((1 << (2 * p + s)) | (1 << (2 * q + s)))
+        for p, q, r, t in itertools.combinations(range(n), 4):
+            if g[p] ^ g[q] ^ g[r] ^ g[t] == 0:
+                out.add((1 << (2 * p + s)) | (1 << (2 * q + s)) | (1 << (2 * r + s)) | (1 << (2 * t + s)))
+    pairs = {}
+    for p, q in itertools.combinations(range(n), 2):
+        pairs.setdefault(g[p] ^ g[q], []).append((1 << (2 * p)) | (1 << (2 * q)))
+    for lab, ups in pairs.items():
+        downs = [m << 1 for m in ups]
+        for u in ups:
+            for d in downs:
+                out.add(u | d)
+    return out
+
+
 def hamiltonian_memory(n_qubits: int, n_groups: int, n_terms: int):
     """Fig. 6(b) vs 6(c) storage (Fig. 9 at PAPER.md:500-504), with
     one byte per boolean entry (reading: the figure's "boolean tuples"):

@@ -67,3 +67,16 @@ def test_from_pauli_spec_example(nnqs):
     assert list(d) == [c1, c2, c3, -c4]
     h = nnqs.nnqs_ham_from_pauli([[0, 0]], [[0, 0]], [-0.8], 4, device=-1)
     assert h.info()["n_groups"] == 1
+
+
+@pytest.mark.parametrize("c", [3, 4, 5])
+def test_flip_mask_set_equals_symmetry_allowed_set(nnqs, c):
+    """P1 at N = 14, 20 and 120: the exported X set is, bit for bit,
+    the symmetry-allowed excitation set written out from the irrep labels
+    (oracle.counts.flip_masks); at N = 20 its N_h is Table 1's N2 value."""
+    m = C.molecule(c)
+    h = nnqs.nnqs_ham_compress(m.h1, m.h2, m.n_qubits, m.e_core, device=-1)
+    x = h.export()[0]
+    got = {int(a) | (int(b) << 64) for a, b in x}
+    assert len(got) == len(x)
+    assert got == counts.flip_masks(m.irreps)
