@@ -414,6 +414,7 @@ def run_ours(args):
 
     # this rank's shard of the unique samples (data-centric)
     b, e = D.shard_bounds(n, world, rank)
+    shard_lens = [e2 - b2 for b2, e2 in (D.shard_bounds(n, world, r) for r in range(world))]
     keys_h = torch.from_numpy(st.keys.view(np.int64)[b:e].copy())
     lp_h = torch.from_numpy(st.logpsi[b:e].copy())
     cnt_h = torch.from_numpy(st.counts[b:e].copy())
@@ -427,17 +428,19 @@ def run_ours(args):
     ev_k = []          # (start, end) events around nnqs_local_energy
 
     def step(kd, ld, cd, timed):
-        if world > 1:
-            gk, gl = D.gather_samples(kd, ld)
-            gc = D.gather_counts(cd)
+        if world > 1:   # every rank knows every shard's size (shard_bounds): no length exchange
+            gk, gl = D.gather_samples(kd, ld, lens=shard_lens)
+            gc = D.gather_counts(cd, lens=shard_lens)
         else:
             gk, gl = kd, ld
         tab = nnqs.nnqs_table_prepare(ham, 0, gk, gl, stream=stream)
         rb, re_ = b, e
         if world > 1:   # contiguous chunk-aligned slice of about equal estimated work
             wk, fl = nnqs.nnqs_chunk_work(tab, stream=stream, with_floor=True)
-            rb, re_ = D.balanced_bounds(wk, world, rank, n_rows=n, floor=fl)
+            bounds = [D.balanced_bounds(wk, world, r, n_rows=n, floor=fl) for r in range(world)]
+            rb, re_ = bounds[rank]
             rows_of["b"], rows_of["e"] = rb, re_
+            rows_of["all"] = [e2 - b2 for b2, e2 in bounds]
         el = eloc[: re_ - rb]
         if timed:
             s0 = torch.cuda.Event(enable_timing=True)
@@ -452,7 +455,7 @@ def run_ours(args):
             s1.record(stream)
             ev_k.append((s0, s1))
         if world > 1:
-            en = D.distributed_energy(el, cnt_rows, stream=stream, p1=p1)
+            en = D.distributed_energy(el, cnt_rows, stream=stream, p1=p1, rows_per_rank=rows_of["all"])
         else:
             m1 = nnqs.nnqs_energy_combine(p1, 1, stream=stream)
             part2 = nnqs.nnqs_energy_chunk_partials(eloc, cd, mean_dev=m1[:2].contiguous(), stream=stream)

@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(LIT_THREADS, 1) k_eloc_lit(HamView H, const Li
     extern __shared__ __align__(128) unsigned char lit_smem[];
     LitRec *tile = reinterpret_cast<LitRec *>(lit_smem);                    // [LIT_STAGES][LIT_TILE]
     __shared__ __align__(8) unsigned long long full[LIT_STAGES], empty[LIT_STAGES];
-    constexpr int kWarps = LIT_THREADS / 32;
+    const int kWarps = blockDim.x / 32;           // blockDim: a multiple of 32, <= LIT_THREADS
     const double s = dkey_inv(*T.shift_key);
     const int64_t K = H.K;
     const int64_t n_tiles = (K + LIT_TILE - 1) / LIT_TILE;
@@ -347,8 +347,8 @@ __global__ void __launch_bounds__(LIT_THREADS, 1) k_eloc_lit(HamView H, const Li
     u64 c_pairs = 0, c_sec = 0, c_hit = 0, c_str = 0;
     // every row block of this CTA streams the whole table: one continuous ring of
     // tiles (global tile counter q = block * n_tiles + t, stage q % S, phase q / S)
-    const int64_t stride = (int64_t)gridDim.x * LIT_THREADS;
-    const int64_t first = (int64_t)blockIdx.x * LIT_THREADS;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t first = (int64_t)blockIdx.x * blockDim.x;
     const int64_t n_blocks = first < n_rows ? (n_rows - first + stride - 1) / stride : 0;
     const int64_t q_end = n_blocks * n_tiles;
     auto issue = [&](int64_t q) {                 // producer: tile q % n_tiles into stage q % S
@@ -691,9 +691,11 @@ int nnqs_launch_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const 
                                  : (cons ? k_eloc_lit<1, true> : k_eloc_lit<1, false>);
         const size_t smem = (size_t)LIT_STAGES * LIT_TILE * sizeof(LitRec);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const int64_t blocks = (n_rows + LIT_THREADS - 1) / LIT_THREADS;
+        // one CTA per SM; fewer threads per CTA when the rows would not fill 148 CTAs
+        const int64_t per = std::min<int64_t>(LIT_THREADS, std::max<int64_t>(64, ((n_rows + 147) / 148 + 31) / 32 * 32));
+        const int64_t blocks = (n_rows + per - 1) / per;
         const int gl = (int)std::min<int64_t>(blocks, 148);
-        kern<<<gl, LIT_THREADS, smem, st>>>(H, (const LitRec *)h->dev.glit, T, row_begin, r, rl, n_rows, o, s, cs);
+        kern<<<gl, (unsigned)per, smem, st>>>(H, (const LitRec *)h->dev.glit, T, row_begin, r, rl, n_rows, o, s, cs);
         return cuda_check(cudaGetLastError(), "local energy launch");
     }
     if (t->mode == 0) {

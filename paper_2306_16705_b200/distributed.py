@@ -137,14 +137,18 @@ def _floor_bounds(w, fl, world):
     return st
 
 
-def all_gather_varlen(t: torch.Tensor, group=None) -> torch.Tensor:
+def all_gather_varlen(t: torch.Tensor, group=None, lens=None) -> torch.Tensor:
     """all_gather_into_tensor of per-rank tensors with different first
-    dimensions: gather the lengths, pad to the maximum, gather, strip."""
+    dimensions: gather the lengths (unless every rank already knows them: `lens`,
+    which saves a collective and a host sync), pad to the maximum, gather, strip."""
     world = dist.get_world_size(group)
-    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
-    ns = torch.empty(world, dtype=torch.int64, device=t.device)
-    dist.all_gather_into_tensor(ns, n, group=group)
-    lens = [int(v) for v in ns.cpu()]
+    if lens is None:
+        n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
+        ns = torch.empty(world, dtype=torch.int64, device=t.device)
+        dist.all_gather_into_tensor(ns, n, group=group)
+        lens = [int(v) for v in ns.cpu()]
+    lens = [int(v) for v in lens]
+    assert lens[dist.get_rank(group)] == t.shape[0], "lens disagrees with this rank's tensor"
     m = max(lens)
     if t.shape[0] < m:
         pad = torch.zeros((m - t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
@@ -167,31 +171,35 @@ def unpack_records(rec: torch.Tensor):
     return keys, logpsi
 
 
-def gather_samples(local_keys: torch.Tensor, local_logpsi: torch.Tensor, group=None):
+def gather_samples(local_keys: torch.Tensor, local_logpsi: torch.Tensor, group=None, lens=None):
     """Stage 2: every rank receives every unique sample.  Shards
-    are disjoint key ranges in rank order, so the concatenation stays sorted."""
-    rec = all_gather_varlen(pack_records(local_keys, local_logpsi), group)
+    are disjoint key ranges in rank order, so the concatenation stays sorted.
+    lens: every rank's shard size, if known everywhere (no length exchange)."""
+    rec = all_gather_varlen(pack_records(local_keys, local_logpsi), group, lens)
     return unpack_records(rec)
 
 
-def gather_counts(local_counts: torch.Tensor, group=None) -> torch.Tensor:
+def gather_counts(local_counts: torch.Tensor, group=None, lens=None) -> torch.Tensor:
     """Sample multiplicities of every rank's shard, in rank order (needed when the
     evaluated row slice, balanced_bounds, differs from the owned sample shard)."""
-    return all_gather_varlen(local_counts.reshape(-1, 1), group).reshape(-1)
+    return all_gather_varlen(local_counts.reshape(-1, 1), group, lens).reshape(-1)
 
 
-def distributed_energy(eloc_local: torch.Tensor, counts_local: torch.Tensor, group=None, stream=None, p1=None):
+def distributed_energy(eloc_local: torch.Tensor, counts_local: torch.Tensor, group=None, stream=None, p1=None,
+                       rows_per_rank=None):
     """Stage 4: count-weighted mean and variance (Eq. 6) over all
     ranks' rows.  p1: this rank's first-pass chunk partials if nnqs_local_energy
-    already produced them (its fused epilogue).  Returns a device f64[4] =
-    (mean_re, mean_im, var, W)."""
+    already produced them (its fused epilogue).  rows_per_rank: every rank's row
+    count, if known everywhere (saves the two length exchanges and host syncs).
+    Returns a device f64[4] = (mean_re, mean_im, var, W)."""
     from . import nnqs
     if p1 is None:
         p1 = nnqs.nnqs_energy_chunk_partials(eloc_local, counts_local, stream=stream)
-    allp = all_gather_varlen(p1[: _n_chunks(eloc_local)], group)
+    clens = None if rows_per_rank is None else [(r + REDUCE_CHUNK - 1) // REDUCE_CHUNK for r in rows_per_rank]
+    allp = all_gather_varlen(p1[: _n_chunks(eloc_local)], group, clens)
     m1 = nnqs.nnqs_energy_combine(allp, 1, stream=stream)
     p2 = nnqs.nnqs_energy_chunk_partials(eloc_local, counts_local, mean_dev=m1[:2].contiguous(), stream=stream)
-    allp2 = all_gather_varlen(p2[: _n_chunks(eloc_local)], group)
+    allp2 = all_gather_varlen(p2[: _n_chunks(eloc_local)], group, clens)
     m2 = nnqs.nnqs_energy_combine(allp2, 2, stream=stream)
     return torch.stack([m1[0], m1[1], m2[0], m1[2]])
 

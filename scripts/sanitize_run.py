@@ -53,11 +53,11 @@ def run(c, n_rows=None, variant="full", **opt):
 
 
 def run_bas():
-    """BAS layers (csrc/bas.cu) on a synthetic 20-orbital model, weights up to 10^12."""
+    """BAS layers (csrc/bas.cu) on a synthetic 20-orbital model, 10^5 samples (~10^5 leaves)."""
     import numpy as np
     dev = torch.device("cuda", 0)
     keys = torch.zeros((1, 2), dtype=torch.int64, device=dev)
-    counts = torch.full((1,), 10**12, dtype=torch.int64, device=dev)
+    counts = torch.full((1,), 10**5, dtype=torch.int64, device=dev)
     rng = np.random.default_rng(3)
     for orbital in range(19, -1, -1):
         probs = torch.from_numpy(rng.random((keys.shape[0], 4)) + 0.01).to(dev)

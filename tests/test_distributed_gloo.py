@@ -64,7 +64,13 @@ def _gather_case(rank, world):
     m = 3 if rank == 0 else 0
     v = D.all_gather_varlen(torch.arange(m * 4, dtype=torch.int64).reshape(m, 4) + 100 * rank)
     ok2 = v.shape == (3, 4) and int(v[0, 0]) == 0
-    return bool(ok and ok2)
+    # every rank knows the lengths: same result without the length exchange
+    lens = [e2 - b2 for b2, e2 in (D.shard_bounds(len(k), world, r) for r in range(world))]
+    gk2, gl2 = D.gather_samples(torch.from_numpy(k[b:e]), torch.from_numpy(lp[b:e]), lens=lens)
+    v2 = D.all_gather_varlen(torch.arange(m * 4, dtype=torch.int64).reshape(m, 4) + 100 * rank,
+                             lens=[3] + [0] * (world - 1))
+    ok3 = np.array_equal(gk2.numpy(), k) and np.array_equal(gl2.numpy(), lp) and torch.equal(v, v2)
+    return bool(ok and ok2 and ok3)
 
 
 def _partials_case(rank, world):
