@@ -8,6 +8,8 @@
 //   energy reduce    Eq. (6) with counts
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include <cmath>
 #include <cstdio>
 
@@ -22,10 +24,13 @@ __constant__ u64 c_hash[128];
 
 namespace {
 
+std::mutex g_hash_ready_mu;
 bool g_hash_ready[64] = {false};
 
+// the hash columns in constant memory of `device` (the current device), once per device
 int ensure_hash(int device) {
     if (device < 0 || device >= 64) return NNQS_E_ARG;
+    std::lock_guard<std::mutex> lk(g_hash_ready_mu);
     if (g_hash_ready[device]) return NNQS_OK;
     u64 cols[128];
     nnqs_hash_columns(cols);

@@ -36,10 +36,13 @@ __constant__ u64 c_hs[128];   // same GF(2) hash columns as kernels.cu (per tran
 
 namespace {
 
+std::mutex g_hs_ready_mu;
 bool g_hs_ready[64] = {false};
 
+// the hash columns in constant memory of `device` (the current device), once per device
 int ensure_hs(int device) {
     if (device < 0 || device >= 64) return NNQS_E_ARG;
+    std::lock_guard<std::mutex> lk(g_hs_ready_mu);
     if (g_hs_ready[device]) return NNQS_OK;
     u64 cols[128];
     nnqs_hash_columns(cols);
@@ -2041,7 +2044,9 @@ void nnqs_spin_index_release(nnqs_ham h) {
 namespace {
 int ensure_binom(int device) {
     static bool ready[64] = {false};
+    static std::mutex mu;
     if (device < 0 || device >= 64) return NNQS_E_ARG;
+    std::lock_guard<std::mutex> lk(mu);
     if (ready[device]) return NNQS_OK;
     static u64 tab[64 * 32];
     for (int p = 0; p < 64; ++p)
