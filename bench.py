@@ -310,7 +310,14 @@ def cpu_baseline(mol, st, n_rows_req, eloc_gpu=None, seconds_target=15.0):
     ref, scale = R.eloc(mol.h1, mol.h2, mol.e_core, st.keys[idx], st.logpsi[idx], keys=st.keys, logpsi=st.logpsi,
                         with_scale=True)
     dt = time.perf_counter() - t0
+    # the same oracle on one host core, on the first rows of the sample
+    m1 = max(8, min(len(idx), int(len(idx) / max(1, threads) * 0.5)))
+    t1 = time.perf_counter()
+    R.eloc(mol.h1, mol.h2, mol.e_core, st.keys[idx[:m1]], st.logpsi[idx[:m1]], keys=st.keys, logpsi=st.logpsi,
+           n_threads=1)
+    single = m1 / (time.perf_counter() - t1)
     out = {"value": len(idx) / dt, "unit": UNIT, "cores": R.num_threads(), "kind": "oracle",
+           "single_core_value": single, "single_core_sample": f"{m1} of the same rows, 1 thread",
            "sample": f"{len(idx)} seeded rows (seed 705) of the {len(st.keys)}-row table, full sample-aware "
                      f"E_loc per row (plain term-by-term Eq. 9 + bisection), {dt:.1f} s"}
     if eloc_gpu is not None:

@@ -531,14 +531,35 @@ __global__ void __launch_bounds__(256) k_chunk_partials(const double2 *eloc, con
     }
 }
 
-__global__ void k_combine(const double *partials, int64_t n_chunks, int pass, double *out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// one block of COMBINE_T threads: thread t sums chunks t, t + T, ... (ascending), then a
+// fixed binary tree -- an order set by the global chunk grid alone (any rank split)
+#define COMBINE_T 1024
+__global__ void __launch_bounds__(COMBINE_T) k_combine(const double *partials, int64_t n_chunks, int pass,
+                                                       double *out) {
+    __shared__ double sw[COMBINE_T], s1[COMBINE_T], s2[COMBINE_T];
+    const int t = threadIdx.x;
     double W = 0.0, S1 = 0.0, S2 = 0.0;
-    for (int64_t c = 0; c < n_chunks; ++c) {     // ascending chunk order
+    for (int64_t c = t; c < n_chunks; c += COMBINE_T) {
         W += partials[3 * c];
         S1 += partials[3 * c + 1];
         S2 += partials[3 * c + 2];
     }
+    sw[t] = W;
+    s1[t] = S1;
+    s2[t] = S2;
+    __syncthreads();
+    for (int h = COMBINE_T / 2; h; h >>= 1) {
+        if (t < h) {
+            sw[t] += sw[t + h];
+            s1[t] += s1[t + h];
+            s2[t] += s2[t + h];
+        }
+        __syncthreads();
+    }
+    if (t != 0) return;
+    W = sw[0];
+    S1 = s1[0];
+    S2 = s2[0];
     if (pass == 1) {
         out[0] = S1 / W; out[1] = S2 / W; out[2] = W; out[3] = 0.0;
     } else {
@@ -749,7 +770,7 @@ extern "C" int nnqs_energy_combine(const double *partials, int64_t n_chunks, int
                                    double *out_dev, void *cuda_stream) {
     if (!partials || !out_dev || n_chunks <= 0 || (pass != 1 && pass != 2))
         return nnqs_set_error(NNQS_E_ARG, "nnqs_energy_combine: bad arguments");
-    k_combine<<<1, 32, 0, (cudaStream_t)cuda_stream>>>(partials, n_chunks, pass, out_dev);
+    k_combine<<<1, COMBINE_T, 0, (cudaStream_t)cuda_stream>>>(partials, n_chunks, pass, out_dev);
     return cuda_check(cudaGetLastError(), "combine launch");
 }
 
@@ -787,9 +808,9 @@ extern "C" int nnqs_energy_reduce(const double *eloc, const int64_t *counts, int
     if (rc) return rc;
     double *part = buf, *o1 = buf + 3 * chunks, *o2 = o1 + 4;
     k_chunk_partials<<<(unsigned)((chunks + 7) / 8), 256, 0, st>>>((const double2 *)eloc, counts, n, nullptr, part);
-    k_combine<<<1, 32, 0, st>>>(part, chunks, 1, o1);
+    k_combine<<<1, COMBINE_T, 0, st>>>(part, chunks, 1, o1);
     k_chunk_partials<<<(unsigned)((chunks + 7) / 8), 256, 0, st>>>((const double2 *)eloc, counts, n, o1, part);
-    k_combine<<<1, 32, 0, st>>>(part, chunks, 2, o2);
+    k_combine<<<1, COMBINE_T, 0, st>>>(part, chunks, 2, o2);
     double h[8];
     rc = cuda_check(cudaMemcpyAsync(h, o1, sizeof(h), cudaMemcpyDeviceToHost, st), "read reduce");
     if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync reduce");

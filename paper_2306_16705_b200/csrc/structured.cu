@@ -368,7 +368,7 @@ template <bool DIRECT, bool OCC, bool AB, bool LOG>
 __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *psi_hat, const double2 *logpsi,
                                              const int2 *q, int qh, int cnt, const RowState *rs, double2 *acc,
                                              const double *occ_rec, int nq, const HitLog &lg, const double *ab_d,
-                                             const ulonglong2 *pair_J, int64_t P) {
+                                             const ulonglong2 *pair_J, int64_t P, const int32_t *listA_idx) {
     const int lane = threadIdx.x & 31;
     uint32_t c_hit = 0, c_str = 0;
     __syncwarp();
@@ -392,6 +392,7 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
                 ge0 = be.y;
             }
         }
+        if (AB && ab && e.x < 0) e.y = __ldg(listA_idx + e.y);   // lazy alpha x beta entry: list position
         if (!direct) ps0 = __ldg(psi_hat + e.y);   // issued with the offsets, used after the sum
         ++c_hit;
     }
@@ -436,13 +437,22 @@ __device__ __forceinline__ uint2 flush_queue(const GroupView &G, const double2 *
             }
         }
         const double hv = flip_sign2(fma(-2.0, sum, Tg), (__popcll(x0 & B0) + __popcll(x1 & B1)) & 1);
-        c_str += __popcll(x0) + __popcll(x1) + 1;
-        add(hv, e.y);
+        if (hv == hv) {                            // NaN: the pair has no group (SpinIndex::occ_rec)
+            c_str += __popcll(x0) + __popcll(x1) + 1;
+            add(hv, e.y);
+        } else {
+            --c_hit;
+        }
     }
     const bool big = lane < cnt && !occ && ge0 - gb0 > 32;
     if (AB && ab) {
-        add(ab_value(ab_d, pair_J, P, ((uint32_t)e.x >> 11) & 0x7FF, (uint32_t)e.x & 0x7FF, x0, x1), e.y);
-        ++c_str;
+        const double hv = ab_value(ab_d, pair_J, P, ((uint32_t)e.x >> 11) & 0x7FF, (uint32_t)e.x & 0x7FF, x0, x1);
+        if (hv == hv) {                            // NaN: no alpha x beta group (lazy entries only)
+            add(hv, e.y);
+            ++c_str;
+        } else {
+            --c_hit;
+        }
     }
     if (lane < cnt && !occ && !big && !ab) {
         // 4 strings in flight per lane (loads issued before the sums; same order)
@@ -505,6 +515,9 @@ __device__ unsigned long long g_prof[16];
 #define WARPS_PER_BLOCK 8
 #ifndef NNQS_AB
 #define NNQS_AB 1      // alpha x beta groups in closed form (SpinIndex::ab_ok)
+#endif
+#ifndef NNQS_LAZY_AB
+#define NNQS_LAZY_AB 1 // light phase (iii) candidates: existence + index resolved in the flush
 #endif
 #ifndef NNQS_SPIN_MINB
 #define NNQS_SPIN_MINB 4
@@ -623,7 +636,7 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
             PROF_T(t_fl)
             const uint2 fo = flush_queue<DIRECT, (PH & 6) != 0, (PH & 8) != 0, LOG>(G, T.psi_hat, T.logpsi, q, qh, cnt, rs, acc,
                                                                                 S.occ_rec, S.nq, T.log, S.ab_d,
-                                                                                S.pair_J, S.P);
+                                                                                S.pair_J, S.P, T.listA_idx);
             c_hit += fo.x;
             c_str += fo.y;
             qh = (qh + cnt) & (QCAP - 1);
@@ -949,8 +962,16 @@ __global__ void __launch_bounds__(256, MINB) k_eloc_spin(SpinView S, GroupView G
                         if (__popcll(d) == 2 && (T.uniform_pc || __popcll(b & d) == 1)) {
                             const int r1 = __ffsll((long long)d) - 1;
                             const int r2 = 63 - __clzll((long long)d);
-                            kk[u] = ab_key(S, ur[u], pair_rank(r1, r2, S.n));
-                            ix[u] = __ldg(T.listA_idx + jj[u]);
+                            if (NNQS_LAZY_AB && S.ab_d) {
+                                // existence and table index resolved at evaluation (no dependent
+                                // load on the scan): the queue carries the alpha-list position
+                                kk[u] = (int32_t)(0x80000000u | AB_TAG | ((uint32_t)ur[u] << 11) |
+                                                  (uint32_t)pair_rank(r1, r2, S.n));
+                                ix[u] = jj[u];
+                            } else {
+                                kk[u] = ab_key(S, ur[u], pair_rank(r1, r2, S.n));
+                                ix[u] = __ldg(T.listA_idx + jj[u]);
+                            }
                         }
                         c_cand += (f0 + 32 * u + lane) < total;
                     }
@@ -1870,7 +1891,10 @@ int nnqs_spin_index_build(const HostTable &H, SpinIndex &S) {
         for (int sp = 0; sp < 2 && S.occ_ok; ++sp)
             for (int64_t rk = 0; rk < S.P && S.occ_ok; ++rk) {
                 const int32_t k = S.pair_k[sp][rk];
-                if (k < 0) continue;
+                if (k < 0) {                        // no group: NaN total, the kernels drop such hits
+                    S.occ_rec[((size_t)sp * S.P + rk) * stride + 2] = std::numeric_limits<double>::quiet_NaN();
+                    continue;
+                }
                 // base B = bitwise majority of the group's strings (the JW string J of
                 // the pair; every other string is J ^ Z_R)
                 int cnt[128] = {0};
