@@ -495,6 +495,8 @@ def run_ours(args):
             a1.synchronize()
             step_ms.append(a0.elapsed_time(a1))
             tab.close()
+            if os.environ.get("NNQS_BENCH_TRACE"):
+                print(f"trace step host_s={time.perf_counter():.4f} dev_ms={step_ms[-1]:.3f}", file=sys.stderr)
         torch.cuda.synchronize()
     clk.__exit__()
     if world > 1:

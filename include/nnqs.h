@@ -130,17 +130,29 @@ int nnqs_ham_free(nnqs_ham h);
  *   thr_double   same-spin lists longer than this are probed (0 = default 8192)
  *   thr_rowheavy alpha groups with more rows than this take phase (iii) through
  *                the entry-driven join (0 = default 16384; raised to thr_single)
+ *   literal_kernel  which kernel runs the literal loop: 0 (NNQS_LIT_AUTO) the
+ *                bit-sliced one (32 rows x 32 groups per sector test, per-spin
+ *                string filter before the lookup) on sample-aware tables of a
+ *                number-conserving H, else the staged one; 1 (NNQS_LIT_STAGED)
+ *                the group-tile-staged one-row-per-thread kernel; 2
+ *                (NNQS_LIT_PLAIN) the unstaged one.  All three visit every
+ *                (row, group) pair in ascending k with the same arithmetic:
+ *                bit-identical results.
  * The thresholds change the work split, never the hit set or a row's value
  * beyond rounding order.  nnqs_options_default fills the defaults.
  */
 #define NNQS_ALGO_AUTO 0
 #define NNQS_ALGO_LITERAL 1
+#define NNQS_LIT_AUTO 0
+#define NNQS_LIT_STAGED 1
+#define NNQS_LIT_PLAIN 2
 typedef struct {
     int32_t algorithm;
     int32_t thr_single;
     int32_t thr_double;
     int32_t thr_rowheavy;
-    int32_t reserved[12];   /* must be zero */
+    int32_t literal_kernel;
+    int32_t reserved[11];   /* must be zero */
 } nnqs_options;
 void nnqs_options_default(nnqs_options *opt);
 

@@ -123,6 +123,11 @@ void nnqs_hash_columns(u64 cols[128]) {
     for (int j = 0; j < 128; ++j) cols[j] = nnqs_splitmix64(s);
 }
 
+void nnqs_filter_columns(uint32_t cols[128]) {
+    u64 s = 0xF117E2306167051ULL;
+    for (int j = 0; j < 128; ++j) cols[j] = (uint32_t)(nnqs_splitmix64(s) >> 32);
+}
+
 u64 nnqs_hash_host(const u64 cols[128], u64 lo, u64 hi) {
     u64 h = 0;
     for (int j = 0; j < 64; ++j)
@@ -239,6 +244,9 @@ int nnqs_table_prepare_ex(nnqs_ham h, int mode, const uint64_t *keys, const doub
             if (r) return nnqs_set_error(NNQS_E_ARG, "nnqs_options.reserved must be zero");
         if (opt->algorithm != NNQS_ALGO_AUTO && opt->algorithm != NNQS_ALGO_LITERAL)
             return nnqs_set_error(NNQS_E_ARG, "nnqs_options.algorithm must be 0 or 1");
+        if (opt->literal_kernel < 0 || opt->literal_kernel > NNQS_LIT_PLAIN)
+            return nnqs_set_error(NNQS_E_ARG, "nnqs_options.literal_kernel must be 0, 1 or 2");
+        o.literal_kernel = opt->literal_kernel;
         if (opt->thr_single < 0 || opt->thr_double < 0 || opt->thr_rowheavy < 0)
             return nnqs_set_error(NNQS_E_ARG, "nnqs_options thresholds must be >= 0");
         o.algorithm = opt->algorithm;

@@ -25,6 +25,9 @@ static inline u64 nnqs_splitmix64(u64 &s) {
     return z ^ (z >> 31);
 }
 void nnqs_hash_columns(u64 cols[128]);
+// 32-bit GF(2)-linear filter hash columns of the bit-sliced literal kernel
+// (per-spin string filters: f_alpha(x) = XOR over the set alpha bits of x, f_beta likewise)
+void nnqs_filter_columns(uint32_t cols[128]);
 u64 nnqs_hash_host(const u64 cols[128], u64 lo, u64 hi);
 
 // ------------------------------------------------------------ Hamiltonian
@@ -102,6 +105,7 @@ struct DeviceHam {
     void *tz = nullptr;       // ulonglong2 Z mask
     double *td = nullptr;     // fused coefficient d
     void *glit = nullptr;     // [K] 32-B {X, h(X), info} records of the literal kernel
+    void *gbs = nullptr;      // [K] 32-B records of the bit-sliced literal kernel (k_eloc_bs), or null
     // spin index (structured path)
     int32_t *pair_k[2] = {nullptr, nullptr};
     int32_t *quad_k[2] = {nullptr, nullptr};
@@ -138,6 +142,7 @@ struct nnqs_table_s {
     void *logpsi = nullptr;   // double2 [n]
     void *psi_hat = nullptr;  // double2 [n]
     u64 *slots = nullptr;     // hash slots [4 * n_buckets] (mode 0)
+    uint32_t *bsbm = nullptr; // alpha- and beta-string filter bitmaps of k_eloc_bs (mode 0)
     u64 bucket_mask = 0;
     u64 *shift_key = nullptr; // device: order-preserving key of s = max Re logpsi
     int *flag = nullptr;      // device: [0] order violation flag, [1] rows with psi_hat(x) < e^-600

@@ -21,6 +21,7 @@
 #define BETA_MASK 0xAAAAAAAAAAAAAAAAULL
 
 __constant__ u64 c_hash[128];
+__constant__ uint32_t c_filt[128];
 
 namespace {
 
@@ -35,6 +36,10 @@ int ensure_hash(int device) {
     u64 cols[128];
     nnqs_hash_columns(cols);
     cudaError_t e = cudaMemcpyToSymbol(c_hash, cols, sizeof(cols));
+    if (e != cudaSuccess) return nnqs_set_error(NNQS_E_CUDA, cudaGetErrorString(e));
+    uint32_t fcols[128];
+    nnqs_filter_columns(fcols);
+    e = cudaMemcpyToSymbol(c_filt, fcols, sizeof(fcols));
     if (e != cudaSuccess) return nnqs_set_error(NNQS_E_CUDA, cudaGetErrorString(e));
     g_hash_ready[device] = true;
     return NNQS_OK;
@@ -477,6 +482,335 @@ __global__ void __launch_bounds__(LIT_THREADS, 1) k_eloc_lit(HamView H, const Li
     }
 }
 
+// ------------------------------ literal Algorithm 2, bit-sliced over rows (v3)
+// The same loop again -- every row x every group, ascending k; sector test,
+// lookup, string sum on a hit -- with the sector test of 32
+// rows x 32 groups done in a few logic instructions.  A warp owns 32 rows and
+// keeps them bit-sliced in shared memory (plane p = bit p of the 32 keys, one
+// word); lane l takes group k0 + l, whose flip mask X_k has at most four bits
+// for a number-conserving H (Eq. 9: singles and doubles), and forms the 32-row
+// mask of rows x with x ^ X_k in x's (N_alpha, N_beta) sector:
+//   one pair per spin   bit_i(x) != bit_j(x)        (P_i ^ P_j)
+//   a pair per spin     (P_i ^ P_j) & (P_k ^ P_l)
+//   a same-spin quad    exactly two of P_i, P_j, P_k, P_l set.
+// The in-sector (group, row) pairs of the 32 x 32 block (~16 % at C5) are then
+// flattened over the warp, 32 at a time in (group, row) order, so every lane has
+// a pair and its lookup in flight: a per-spin string filter (f_alpha(x'),
+// f_beta(x') in shared-memory bitmaps of the table's alpha and beta strings --
+// GF(2)-linear, f(x ^ X) = f(x) ^ f(X); no false negatives), then the hash
+// probe of Algorithm 2's lookup, then, on a hit, the string sum.  Each row's
+// lane adds its hits in ascending k with the same arithmetic as k_eloc_v1, so
+// the result is bit-identical to it.
+#ifndef BS_WARPS
+#define BS_WARPS 16
+#endif
+#ifndef BS_TILE
+#define BS_TILE 256
+#endif
+#ifndef BS_STAGES
+#define BS_STAGES 4
+#endif
+#define BS_FB 19                                  // filter bits per spin (2^19-bit bitmaps, 64 KB each)
+#define BS_BM_WORDS (2u << (BS_FB - 5))           // both bitmaps, 32-bit words
+#define BS_SMEM ((size_t)BS_BM_WORDS * 4 + (size_t)BS_STAGES * BS_TILE * sizeof(BsRec))
+
+struct BsRec {
+    ulonglong2 x;      // X_k
+    u64 hx;            // h(X_k)
+    uint32_t fa, fb;   // f_alpha(X_k), f_beta(X_k)
+    uint32_t pos;      // flip sites, alpha ones first; 128 = the zero plane, 129 = the ones plane
+    uint32_t sb;       // strings [sb, se) of group k
+    uint32_t se;       // bit 31: same-spin quad (two-of-four test)
+    uint32_t pad;
+};
+
+// Algorithm 2's lookup of x' (the probe above) with the common case -- an absent key
+// whose first bucket has an empty slot and no fingerprint match -- decided from one
+// 32-B load without a loop
+__device__ __forceinline__ int64_t probe_fast(const TabView &T, u64 h, u64 p0, u64 p1) {
+    const u64 b = h & T.bucket_mask;
+    const uint32_t fp = (uint32_t)(h >> 32);
+    const ulonglong2 *bk = reinterpret_cast<const ulonglong2 *>(T.slots + 4 * b);
+    const ulonglong2 s01 = __ldg(bk), s23 = __ldg(bk + 1);
+    const bool m0 = (uint32_t)(s01.x >> 32) == fp && s01.x != NNQS_EMPTY_SLOT;
+    const bool m1 = (uint32_t)(s01.y >> 32) == fp && s01.y != NNQS_EMPTY_SLOT;
+    const bool m2 = (uint32_t)(s23.x >> 32) == fp && s23.x != NNQS_EMPTY_SLOT;
+    const bool m3 = (uint32_t)(s23.y >> 32) == fp && s23.y != NNQS_EMPTY_SLOT;
+    if (!(m0 | m1 | m2 | m3) && s23.y == NNQS_EMPTY_SLOT) return -1;   // slots fill in order
+    return probe(T, h, p0, p1);
+}
+
+__device__ __forceinline__ uint32_t ffilt(u64 w, int base) {
+    uint32_t f = 0;
+    while (w) {
+        f ^= c_filt[base + __ffsll((long long)w) - 1];
+        w &= w - 1;
+    }
+    return f;
+}
+
+__device__ __forceinline__ bool bm_test(const uint32_t *bm, uint32_t f) {
+    const uint32_t b = f & ((1u << BS_FB) - 1);
+    return (bm[b >> 5] >> (b & 31)) & 1u;
+}
+
+__global__ void __launch_bounds__(BS_WARPS * 32, 1) k_eloc_bs(HamView H, const BsRec *rec, TabView T,
+                                                              const uint32_t *bm, int64_t row_begin,
+                                                              const ulonglong2 *rows, const double2 *row_lp,
+                                                              int64_t n_rows, double2 *out,
+                                                              unsigned long long *stats, ChunkSink cs) {
+    extern __shared__ __align__(128) unsigned char bs_smem[];
+    uint32_t *s_bm = reinterpret_cast<uint32_t *>(bs_smem);                          // [2][2^BS_FB / 32]
+    BsRec *tile = reinterpret_cast<BsRec *>(bs_smem + (size_t)BS_BM_WORDS * 4);    // [BS_STAGES][BS_TILE]
+    __shared__ uint32_t s_pl[BS_WARPS][130];        // bit planes of the warp's 32 rows (+ zero, ones)
+    __shared__ ulonglong2 s_rx[BS_WARPS][32];       // the warp's rows: key
+    __shared__ uint4 s_rh[BS_WARPS][32];            //   h(x) lo, hi, f_alpha(x), f_beta(x)
+    __shared__ double2 s_rl[BS_WARPS][32];          //   log psi(x)
+    __shared__ double s_qh[BS_WARPS][32];           // hits of one round: H_xx', psi-hat ratio, row
+    __shared__ double2 s_qp[BS_WARPS][32];
+    __shared__ int32_t s_qr[BS_WARPS][32];
+    __shared__ __align__(8) unsigned long long full[BS_STAGES];
+    __shared__ unsigned s_done[BS_STAGES];          // warps done with the stage's current tile
+    const int kWarps = blockDim.x / 32;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned FULL = 0xffffffffu;
+    const double s = dkey_inv(*T.shift_key);
+    const int64_t K = H.K;
+    const int64_t n_tiles = (K + BS_TILE - 1) / BS_TILE;
+    u64 c_pairs = 0, c_sec = 0, c_hit = 0, c_str = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t first = (int64_t)blockIdx.x * blockDim.x;
+    const int64_t n_blocks = first < n_rows ? (n_rows - first + stride - 1) / stride : 0;
+    const int64_t q_end = n_blocks * n_tiles;
+    auto issue = [&](int64_t q) {
+        const int st = (int)(q % BS_STAGES);
+        const int64_t g0 = (q % n_tiles) * BS_TILE;
+        const unsigned bytes = (unsigned)(min((int64_t)BS_TILE, K - g0) * (int64_t)sizeof(BsRec));
+        mbar_expect_tx(&full[st], bytes);
+        bulk_g2s(tile + st * BS_TILE, rec + g0, bytes, &full[st]);
+    };
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < BS_STAGES; ++st) {
+            mbar_init(&full[st], 1);
+            s_done[st] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (uint32_t i = threadIdx.x; i < BS_BM_WORDS / 4; i += blockDim.x)
+        reinterpret_cast<uint4 *>(s_bm)[i] = __ldg(reinterpret_cast<const uint4 *>(bm) + i);
+    if (lane == 0) {
+        s_pl[wid][128] = 0u;
+        s_pl[wid][129] = ~0u;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int64_t q = 0; q < BS_STAGES && q < q_end; ++q) issue(q);
+    const uint32_t *bmA = s_bm, *bmB = s_bm + BS_BM_WORDS / 2;
+    uint32_t *pl = s_pl[wid];
+    int64_t q = 0;
+    for (int64_t blk = 0; blk < n_blocks; ++blk) {
+        const int64_t r = first + blk * stride + threadIdx.x;
+        u64 x0 = 0, x1 = 0;
+        double2 lx = make_double2(-INFINITY, 0.0);
+        if (r < n_rows) {
+            if (rows) {
+                const ulonglong2 k = rows[r];
+                x0 = k.x;
+                x1 = k.y;
+                lx = row_lp[r];
+            } else {
+                const ulonglong2 k = T.keys[row_begin + r];
+                x0 = k.x;
+                x1 = k.y;
+                lx = T.logpsi[row_begin + r];
+            }
+        }
+        const bool live = lx.x > -INFINITY;      // psi(x) = 0 (reading R10) or past the end: no pairs
+        const uint32_t live_m = __ballot_sync(FULL, live);
+        __syncwarp();
+        {
+            const u64 hx = live ? hash128(x0, x1) : 0;
+            const uint32_t fa = live ? ffilt(x0 & ALPHA_MASK, 0) ^ ffilt(x1 & ALPHA_MASK, 64) : 0;
+            const uint32_t fb = live ? ffilt(x0 & BETA_MASK, 0) ^ ffilt(x1 & BETA_MASK, 64) : 0;
+            s_rx[wid][lane] = make_ulonglong2(x0, x1);
+            s_rh[wid][lane] = make_uint4((uint32_t)hx, (uint32_t)(hx >> 32), fa, fb);
+            s_rl[wid][lane] = lx;
+        }
+        for (int p = 0; p < 128; ++p) {          // bit planes of the warp's rows
+            const uint32_t v = __ballot_sync(FULL, ((p < 64 ? x0 >> p : x1 >> (p - 64)) & 1ULL) != 0);
+            if (lane == (p & 31)) pl[p] = v;
+        }
+        __syncwarp();
+        double ar = 0.0, ai = 0.0;
+        for (int64_t t = 0; t < n_tiles; ++t, ++q) {
+            const int st = (int)(q % BS_STAGES);
+            const unsigned ph = (unsigned)((q / BS_STAGES) & 1);
+            mbar_wait(&full[st], ph);
+            const BsRec *tl = tile + st * BS_TILE;
+            const int gn = live_m ? (int)min((int64_t)BS_TILE, K - t * BS_TILE) : 0;
+            for (int g0 = 0; g0 < gn; g0 += 32) {
+                // lane = group g0 + lane: the 32-row in-sector mask
+                uint32_t m = 0;
+                if (g0 + lane < gn) {
+                    const uint32_t pos = tl[g0 + lane].pos, se = tl[g0 + lane].se;
+                    const uint32_t P0 = pl[pos & 0xff], P1 = pl[(pos >> 8) & 0xff];
+                    const uint32_t P2 = pl[(pos >> 16) & 0xff], P3 = pl[pos >> 24];
+                    const uint32_t s1 = P0 ^ P1, s2 = P2 ^ P3;
+                    if (se >> 31) m = (s1 & s2) | (((P0 & P1) ^ (P2 & P3)) & ~(s1 | s2));
+                    else m = s1 & s2;
+                    m &= live_m;
+                }
+                // the in-sector (group, row) pairs, flattened over the warp in (group, row) order
+                const int cnt = __popc(m);
+                int incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                const int excl = incl - cnt;
+                const int total = __shfl_sync(FULL, incl, 31);
+                c_sec += cnt;
+                for (int f0 = 0; f0 < total; f0 += 32) {
+                    const int f = f0 + lane;
+                    int lo = 0;                          // owner: the last lane with excl <= f
+#pragma unroll
+                    for (int sp = 16; sp; sp >>= 1) {
+                        const int cnd = lo + sp;
+                        const int ex = __shfl_sync(FULL, excl, cnd & 31);
+                        if (cnd < 32 && ex <= f) lo = cnd;
+                    }
+                    const uint32_t mo = __shfl_sync(FULL, m, lo);
+                    const int exo = __shfl_sync(FULL, excl, lo);
+                    int64_t idx = -1;
+                    int row = 0;
+                    if (f < total) {
+                        int k = f - exo;                 // row = the k-th set bit of mo
+                        uint32_t v = mo;
+#pragma unroll
+                        for (int sh = 16; sh; sh >>= 1) {
+                            const int c = __popc(v & ((1u << sh) - 1u));
+                            if (k >= c) {
+                                k -= c;
+                                v >>= sh;
+                                row += sh;
+                            }
+                        }
+                        const uint4 rh = s_rh[wid][row];
+                        const BsRec &G = tl[g0 + lo];
+                        if (bm_test(bmA, rh.z ^ G.fa) && bm_test(bmB, rh.w ^ G.fb)) {
+                            const ulonglong2 xr = s_rx[wid][row];
+                            const ulonglong2 X = G.x;
+                            const u64 hxr = (u64)rh.x | ((u64)rh.y << 32);
+                            idx = probe_fast(T, hxr ^ G.hx, xr.x ^ X.x, xr.y ^ X.y);
+                        }
+                    }
+                    const unsigned hm = __ballot_sync(FULL, idx >= 0);
+                    if (hm) {                            // rare: ~0.4 hits per 32 x 32 pairs at C5
+                        if (idx >= 0) {                  // H_xx' (strings in order) and psi(x')/psi-hat
+                            const BsRec &G = tl[g0 + lo];
+                            const ulonglong2 xr = s_rx[wid][row];
+                            const uint32_t b = G.sb, e = G.se & 0x7FFFFFFFu;
+                            double hv = 0.0;
+                            for (uint32_t i = b; i < e; ++i) {
+                                const ulonglong2 Z = __ldg(H.tz + i);
+                                const int par = (__popcll(xr.x & Z.x) + __popcll(xr.y & Z.y)) & 1;
+                                hv += flip_sign(__ldg(H.td + i), par);
+                            }
+                            c_str += e - b;
+                            const double2 lr = s_rl[wid][row];
+                            double2 ps;
+                            if (!((lr.x - s) < -600.0)) {
+                                ps = __ldg(T.psi_hat + idx);
+                            } else {
+                                const double2 l = T.logpsi[idx];
+                                const double mm = exp(l.x - lr.x);
+                                double sn, cs2;
+                                sincos(l.y - lr.y, &sn, &cs2);
+                                ps = make_double2(mm * cs2, mm * sn);
+                            }
+                            s_qh[wid][lane] = hv;
+                            s_qp[wid][lane] = ps;
+                            s_qr[wid][lane] = row;
+                        }
+                        __syncwarp();
+                        unsigned h2 = hm;                // each row adds its hits in (group) order
+                        while (h2) {
+                            const int l = __ffs(h2) - 1;
+                            h2 &= h2 - 1;
+                            if (s_qr[wid][l] == lane) {
+                                const double hv = s_qh[wid][l];
+                                const double2 ps = s_qp[wid][l];
+                                ar = fma(hv, ps.x, ar);
+                                ai = fma(hv, ps.y, ai);
+                                ++c_hit;
+                            }
+                        }
+                        __syncwarp();
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {                         // the last warp done with the tile refills the stage
+                __threadfence_block();
+                if (atomicAdd(&s_done[st], 1u) == (unsigned)kWarps - 1) {
+                    s_done[st] = 0;
+                    if (q + BS_STAGES < q_end) {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        issue(q + BS_STAGES);
+                    }
+                }
+            }
+        }
+        if (r < n_rows) {
+            double2 e;
+            if (!live) {
+                e = make_double2(NAN, NAN);
+            } else if ((lx.x - s) < -600.0) {
+                e = make_double2(ar, ai);
+            } else {
+                // E = acc / psi_hat(x) = acc * exp(-(logpsi(x) - s))
+                const double mm = exp(-(lx.x - s));
+                double sn, cs2;
+                sincos(-lx.y, &sn, &cs2);
+                const double ir = mm * cs2, ii = mm * sn;
+                e = make_double2(ar * ir - ai * ii, ar * ii + ai * ir);
+            }
+            if (live) c_pairs += (u64)K;
+            out[r] = e;
+            chunk_done_thread(cs, out, r, n_rows);
+        }
+        __syncwarp();                                // row arrays reused by the next block
+    }
+    if (stats) {
+        for (int o = 16; o; o >>= 1) {
+            c_pairs += __shfl_xor_sync(0xffffffffu, c_pairs, o);
+            c_sec += __shfl_xor_sync(0xffffffffu, c_sec, o);
+            c_hit += __shfl_xor_sync(0xffffffffu, c_hit, o);
+            c_str += __shfl_xor_sync(0xffffffffu, c_str, o);
+        }
+        if (lane == 0) {
+            atomicAdd(stats + 0, c_pairs);
+            atomicAdd(stats + 1, c_sec);
+            atomicAdd(stats + 2, c_hit);
+            atomicAdd(stats + 3, c_str);
+        }
+    }
+}
+
+// per-spin string filter bitmaps of a mode-0 table (k_eloc_bs): bit f_alpha(key) and bit f_beta(key)
+__global__ void k_bs_bitmap(const ulonglong2 *keys, int64_t n, uint32_t *bm) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const ulonglong2 k = keys[i];
+        const uint32_t fa = ffilt(k.x & ALPHA_MASK, 0) ^ ffilt(k.y & ALPHA_MASK, 64);
+        const uint32_t fb = ffilt(k.x & BETA_MASK, 0) ^ ffilt(k.y & BETA_MASK, 64);
+        const uint32_t ba = fa & ((1u << BS_FB) - 1), bb = fb & ((1u << BS_FB) - 1);
+        atomicOr(bm + (ba >> 5), 1u << (ba & 31));
+        atomicOr(bm + BS_BM_WORDS / 2 + (bb >> 5), 1u << (bb & 31));
+    }
+}
+
 template <int MODE, bool CONS>
 __global__ void k_coupled_debug(HamView H, TabView T, const ulonglong2 *rows, int64_t n_rows,
                                 int64_t max_pairs, int64_t *oi, u64 *ox, double *oh,
@@ -628,7 +962,43 @@ int nnqs_ham_upload(nnqs_ham h) {
     const size_t bl = sizeof(LitRec) * lit.size();
     if ((rc = cuda_check(cudaMalloc(&D.glit, bl), "cudaMalloc glit"))) return rc;
     if ((rc = cuda_check(cudaMemcpy(D.glit, lit.data(), bl, cudaMemcpyHostToDevice), "copy glit"))) return rc;
-    D.bytes = (int64_t)(bx + bh + bi + bo + bz + bd + bl);
+    // the bit-sliced kernel's records: only when every flip mask has at most four
+    // sites with an even count per spin (a number-conserving H: Eq. 9's singles and
+    // doubles), so the 32-row sector test is one of the three forms of k_eloc_bs
+    size_t bb = 0;
+    bool bs_ok = H.conserving && K > 0 && Nh < 0x7FFFFFFFLL;
+    for (int64_t k = 0; k < K && bs_ok; ++k) {
+        const u64 x0 = H.x[2 * k], x1 = H.x[2 * k + 1];
+        const int na = __builtin_popcountll(x0 & ALPHA_MASK) + __builtin_popcountll(x1 & ALPHA_MASK);
+        const int nb = __builtin_popcountll(x0 & BETA_MASK) + __builtin_popcountll(x1 & BETA_MASK);
+        bs_ok = (na & 1) == 0 && (nb & 1) == 0 && na + nb <= 4;
+    }
+    if (bs_ok) {
+        uint32_t fcol[128];
+        nnqs_filter_columns(fcol);
+        std::vector<BsRec> bs(K);
+        for (int64_t k = 0; k < K; ++k) {
+            const u64 x[2] = {H.x[2 * k], H.x[2 * k + 1]};
+            uint32_t fa = 0, fb = 0, pos = 0;
+            int np = 0, na = 0;
+            for (int spin = 0; spin < 2; ++spin)          // alpha sites (even qubits) first
+                for (int j = 0; j < 128; ++j)
+                    if ((x[j >> 6] >> (j & 63) & 1) && (j & 1) == spin) {
+                        (spin ? fb : fa) ^= fcol[j];
+                        pos |= (uint32_t)j << (8 * np++);
+                        na += spin == 0;
+                    }
+            const bool quad = na == 4 || np - na == 4;
+            if (np == 0) pos = 128u | 129u << 8 | 128u << 16 | 129u << 24;
+            else if (np == 2) pos |= 128u << 16 | 129u << 24;
+            bs[k] = BsRec{make_ulonglong2(x[0], x[1]), hx[k], fa, fb, pos, off[k],
+                          off[k + 1] | (quad ? 0x80000000u : 0u), 0};
+        }
+        bb = sizeof(BsRec) * bs.size();
+        if ((rc = cuda_check(cudaMalloc(&D.gbs, bb), "cudaMalloc gbs"))) return rc;
+        if ((rc = cuda_check(cudaMemcpy(D.gbs, bs.data(), bb, cudaMemcpyHostToDevice), "copy gbs"))) return rc;
+    }
+    D.bytes = (int64_t)(bx + bh + bi + bo + bz + bd + bl + bb);
     return NNQS_OK;
 }
 
@@ -636,6 +1006,7 @@ void nnqs_ham_release(nnqs_ham h) {
     DeviceHam &D = h->dev;
     cudaFree(D.gx); cudaFree(D.ghx); cudaFree(D.ginfo); cudaFree(D.goff); cudaFree(D.tz); cudaFree(D.td);
     cudaFree(D.glit);
+    cudaFree(D.gbs);
     D = DeviceHam();
 }
 
@@ -666,8 +1037,12 @@ int nnqs_table_build(nnqs_table t, const uint64_t *keys, const double *logpsi, v
         }
         if ((rc = cuda_check(cudaMemsetAsync(t->slots, 0xFF, 32 * nb, st), "memset slots"))) return rc;
         t->bytes += (int64_t)bk + 32 * (int64_t)nb;
+        if ((rc = cuda_check(nnqs_malloc_async((void **)&t->bsbm, 4 * (size_t)BS_BM_WORDS, st), "alloc bsbm"))) return rc;
+        if ((rc = cuda_check(cudaMemsetAsync(t->bsbm, 0, 4 * (size_t)BS_BM_WORDS, st), "memset bsbm"))) return rc;
+        t->bytes += 4 * (int64_t)BS_BM_WORDS;
         if (n > 1) k_check_order<<<grid_for(n, 256), 256, 0, st>>>((const ulonglong2 *)t->keys, n, t->flag);
         if (n) k_hash_insert<<<grid_for(n, 256), 256, 0, st>>>((const ulonglong2 *)t->keys, n, t->slots, t->bucket_mask);
+        if (n) k_bs_bitmap<<<grid_for(n, 256), 256, 0, st>>>((const ulonglong2 *)t->keys, n, t->bsbm);
     }
     if (n) {
         k_max_re<<<grid_for(n, 256), 256, 0, st>>>((const double2 *)t->logpsi, n, t->shift_key);
@@ -691,6 +1066,8 @@ void nnqs_table_release(nnqs_table t) {
     if (t->logpsi) cudaFreeAsync(t->logpsi, st);
     if (t->psi_hat) cudaFreeAsync(t->psi_hat, st);
     if (t->slots) cudaFreeAsync(t->slots, st);
+    if (t->bsbm) cudaFreeAsync(t->bsbm, st);
+    t->bsbm = nullptr;
     if (t->shift_key) cudaFreeAsync(t->shift_key, st);
     t->keys = t->logpsi = t->psi_hat = nullptr;
     t->slots = t->shift_key = nullptr;
@@ -709,10 +1086,18 @@ int nnqs_launch_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const 
     auto *rl = (const double2 *)row_logpsi;
     auto *o = (double2 *)eloc;
     auto *s = (unsigned long long *)stats;
-#ifndef NNQS_LIT_V1
-#define NNQS_LIT_V1 0                             // A/B builds only: the unstaged k_eloc_v1
-#endif
-    if (h->dev.glit && !NNQS_LIT_V1) {            // staged literal kernel (k_eloc_lit)
+    const int lk = t->opt.literal_kernel;
+    if (lk == NNQS_LIT_AUTO && t->mode == 0 && cons && h->dev.gbs && t->bsbm) {   // bit-sliced (k_eloc_bs)
+        cudaFuncSetAttribute(k_eloc_bs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BS_SMEM);
+        // one CTA per SM, 32 rows per warp; fewer warps per CTA when the rows would not fill 148 CTAs
+        const int64_t warps_needed = (n_rows + 31) / 32;
+        const int64_t per = std::min<int64_t>(BS_WARPS, std::max<int64_t>(1, (warps_needed + 147) / 148)) * 32;
+        const int gl = (int)std::min<int64_t>((n_rows + per - 1) / per, 148);
+        k_eloc_bs<<<gl, (unsigned)per, BS_SMEM, st>>>(H, (const BsRec *)h->dev.gbs, T, t->bsbm, row_begin, r, rl,
+                                                       n_rows, o, s, cs);
+        return cuda_check(cudaGetLastError(), "local energy launch");
+    }
+    if (h->dev.glit && lk != NNQS_LIT_PLAIN) {    // staged literal kernel (k_eloc_lit)
         auto kern = t->mode == 0 ? (cons ? k_eloc_lit<0, true> : k_eloc_lit<0, false>)
                                  : (cons ? k_eloc_lit<1, true> : k_eloc_lit<1, false>);
         const size_t smem = (size_t)LIT_STAGES * LIT_TILE * sizeof(LitRec);

@@ -52,7 +52,8 @@ _sig = {
 class Options(ctypes.Structure):
     """nnqs_options (include/nnqs.h): per-table algorithm and list thresholds."""
     _fields_ = [("algorithm", ctypes.c_int32), ("thr_single", ctypes.c_int32), ("thr_double", ctypes.c_int32),
-                ("thr_rowheavy", ctypes.c_int32), ("reserved", ctypes.c_int32 * 12)]
+                ("thr_rowheavy", ctypes.c_int32), ("literal_kernel", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 11)]
 
 
 for _name, (_args, _res) in _sig.items():
@@ -204,18 +205,20 @@ def nnqs_options_default() -> Options:
 
 
 def nnqs_table_prepare(ham: Hamiltonian, mode: int, keys, logpsi, stream=None, algorithm: int | None = None,
-                       thr_single: int = 0, thr_double: int = 0, thr_rowheavy: int = 0) -> Table:
+                       thr_single: int = 0, thr_double: int = 0, thr_rowheavy: int = 0,
+                       literal_kernel: int = 0) -> Table:
     """keys: CUDA int64/uint64 [n, 2] (mode 0) or None (mode 1); logpsi CUDA float64 [n, 2].
     Keyword options fill nnqs_options (0 = the library default) -> nnqs_table_prepare_ex."""
     n = int(logpsi.shape[0])
     out = P()
-    if algorithm is None and not (thr_single or thr_double or thr_rowheavy):
+    if algorithm is None and not (thr_single or thr_double or thr_rowheavy or literal_kernel):
         _check(_lib.nnqs_table_prepare(ham.handle, int(mode), _dev_ptr(keys), _dev_ptr(logpsi), n, _stream(stream),
                                        ctypes.byref(out)))
     else:
         o = Options()
         o.algorithm = int(algorithm or 0)
         o.thr_single, o.thr_double, o.thr_rowheavy = int(thr_single), int(thr_double), int(thr_rowheavy)
+        o.literal_kernel = int(literal_kernel)
         _check(_lib.nnqs_table_prepare_ex(ham.handle, int(mode), _dev_ptr(keys), _dev_ptr(logpsi), n,
                                           ctypes.byref(o), _stream(stream), ctypes.byref(out)))
     return Table(out, mode, n)

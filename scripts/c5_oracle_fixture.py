@@ -44,17 +44,18 @@ def part_order(n_parts: int) -> np.ndarray:
     return np.random.default_rng(705).permutation(n_parts)
 
 
-def run(threads: int, max_parts: int) -> None:
+def run(threads: int, max_parts: int, reverse: bool = False, parts_dir: str = PARTS_DIR) -> None:
     mol = C.molecule(5)
     st = C.sample_table(5)
     n = len(st.keys)
-    os.makedirs(PARTS_DIR, exist_ok=True)
+    os.makedirs(parts_dir, exist_ok=True)
     dig = input_digest(st)
     n_parts = (n + PART - 1) // PART
     done = 0
-    for p in part_order(n_parts):
-        path = os.path.join(PARTS_DIR, f"part_{p:04d}.npz")
-        if os.path.exists(path):
+    order = part_order(n_parts)
+    for p in (order[::-1] if reverse else order):   # two workers: one from each end
+        path = os.path.join(parts_dir, f"part_{p:04d}.npz")
+        if os.path.exists(path) or os.path.exists(os.path.join(PARTS_DIR, f"part_{p:04d}.npz")):
             continue
         if done >= max_parts:
             break
@@ -66,7 +67,7 @@ def run(threads: int, max_parts: int) -> None:
         np.savez(tmp, r0=r0, r1=r1, re=e.real, im=e.imag, scale=s, digest=dig)
         os.replace(tmp, path)
         done += 1
-        have = len([f for f in os.listdir(PARTS_DIR) if f.startswith("part_") and f.endswith(".npz")])
+        have = len([f for f in os.listdir(parts_dir) if f.startswith("part_") and f.endswith(".npz")])
         print(f"part {p} rows [{r0},{r1}) {time.time() - t0:.1f}s  ({have}/{n_parts})", flush=True)
 
 
@@ -102,8 +103,10 @@ if __name__ == "__main__":
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--max-parts", type=int, default=1 << 30)
     ap.add_argument("--merge", action="store_true")
+    ap.add_argument("--reverse", action="store_true", help="walk the part order from its end (a second worker)")
+    ap.add_argument("--parts-dir", default=PARTS_DIR, help="where new parts go (merge reads tests/golden/c5_parts)")
     a = ap.parse_args()
     if a.merge:
         merge()
     else:
-        run(a.threads, a.max_parts)
+        run(a.threads, a.max_parts, a.reverse, a.parts_dir)

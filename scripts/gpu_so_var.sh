@@ -5,6 +5,6 @@ cp paper_2306_16705_b200/libnnqs.so /tmp/libnnqs_orig.so
 for f in ${SO_VARIANTS:-variants/*.so}; do
   cp "$f" paper_2306_16705_b200/libnnqs.so
   echo "== $f" >> gpurun_out/sovar.txt
-  timeout 300 python scripts/time_kernel.py 5 2>&1 | grep -v "^compress" >> gpurun_out/sovar.txt
+  timeout 300 python scripts/time_kernel.py ${TK_ARGS:-5} 2>&1 | grep -v "^compress" >> gpurun_out/sovar.txt
 done
 cp /tmp/libnnqs_orig.so paper_2306_16705_b200/libnnqs.so

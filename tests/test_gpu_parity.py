@@ -718,3 +718,71 @@ def test_bench_two_ranks_shared_gpu():
     one, two = run(1), run(2)
     assert one["energy"] == two["energy"]
     assert one["stats"]["hits"] == two["stats"]["hits"]
+
+
+# ------------------------------------- literal loop: the three kernels agree bit for bit
+def _lit_run(nnqs, ham, tab, dev, lk, n=None, rows=None, rlp=None, row_begin=0):
+    stats = torch.zeros(4, dtype=torch.int64, device=dev)
+    if rows is None:
+        el = nnqs.nnqs_local_energy(ham, tab, row_begin, n_rows=n, stats_out=stats)
+    else:
+        el = nnqs.nnqs_local_energy(ham, tab, rows=_t(rows, dev), row_logpsi=_t(rlp, dev), stats_out=stats)
+    return el.cpu().numpy(), stats.cpu().numpy()
+
+
+@pytest.mark.parametrize("c,variant", [(2, "half"), (3, "full"), (3, "half"), (4, "full")])
+def test_literal_kernels_bit_identical(nnqs, dev, c, variant):
+    """Algorithm 2's loop in its three kernels -- bit-sliced (32 rows x 32
+    groups per sector test + per-spin string filter), group-tile staged, plain -- gives
+    the same bits and the same pair / in-sector / hit / string counts, on table rows
+    (a psi = 0 row and a row on the exp-ratio path, R10/R11, included), on explicit
+    rows that are not in the table, and on a ragged slice; and matches the oracle (R14)."""
+    m = C.molecule(c)
+    st = C.sample_table(c, variant)
+    lp = st.logpsi.copy()
+    lp[3, 0] = -np.inf
+    lp[5, 0] -= 620.0
+    ham = ham_for(nnqs, c)
+    full = C.sample_table(c, "full")
+    rows, rlp = full.keys, full.logpsi          # for "half": rows outside the table too
+    outs = []
+    for lk in (0, 1, 2):
+        tab = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(lp, dev), algorithm=nnqs.ALGO_LITERAL,
+                                      literal_kernel=lk)
+        n = len(st.keys)
+        a = _lit_run(nnqs, ham, tab, dev, lk, n=n)
+        b = _lit_run(nnqs, ham, tab, dev, lk, rows=rows, rlp=rlp)
+        cut = 1 + n // 3
+        d = _lit_run(nnqs, ham, tab, dev, lk, n=n - cut - 1, row_begin=cut)
+        outs.append((a, b, d))
+    for (a, b, d) in outs[1:]:
+        for u, v in zip((a, b, d), outs[0]):
+            assert u[0].tobytes() == v[0].tobytes()
+            assert np.array_equal(u[1], v[1])
+    el = outs[0][0][0]
+    got = el[:, 0] + 1j * el[:, 1]
+    ok = np.isfinite(lp[:, 0])
+    assert np.all(np.isnan(got[~ok].real))
+    ref, scale = R.eloc(m.h1, m.h2, m.e_core, st.keys[ok], lp[ok], keys=st.keys, logpsi=lp, with_scale=True)
+    _assert_close(got[ok], ref, scale, f"C{c}/{variant} bit-sliced literal")
+
+
+def test_c5_literal_kernels_bit_identical(nnqs, dev, c5):
+    """C5 (120 qubits, 2.06M groups): a ragged 2085-row slice plus the HF row and the
+    10 longest-list rows as explicit rows -- bit-sliced == staged, bit for bit, equal
+    counts, and the oracle's E_loc within R14."""
+    m, st, ham, _ = c5
+    hf, top, _ = _c5_special_rows(st)
+    idx = np.unique(np.concatenate([np.arange(2085), [hf], top]))
+    rows, rlp = st.keys[idx], st.logpsi[idx]
+    res = []
+    for lk in (0, 1):
+        tab = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(st.logpsi, dev), algorithm=nnqs.ALGO_LITERAL,
+                                      literal_kernel=lk)
+        res.append(_lit_run(nnqs, ham, tab, dev, lk, rows=rows, rlp=rlp))
+        tab.close()
+    assert res[0][0].tobytes() == res[1][0].tobytes() and np.array_equal(res[0][1], res[1][1])
+    sub = np.unique(np.concatenate([C.oracle_row_subset(5, len(idx), 24), np.searchsorted(idx, [hf])]))
+    got = res[0][0][sub, 0] + 1j * res[0][0][sub, 1]
+    ref, scale = R.eloc(m.h1, m.h2, m.e_core, rows[sub], rlp[sub], keys=st.keys, logpsi=st.logpsi, with_scale=True)
+    _assert_close(got, ref, scale, "C5 bit-sliced literal")
