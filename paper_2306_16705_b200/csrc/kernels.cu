@@ -510,9 +510,12 @@ __global__ void __launch_bounds__(LIT_THREADS, 1) k_eloc_lit(HamView H, const Li
 #ifndef BS_STAGES
 #define BS_STAGES 4
 #endif
+#ifndef BS_P
+#define BS_P 1                                    // 32-row blocks per warp (2 and 4 measured slower)
+#endif
 #define BS_FB 19                                  // filter bits per spin (2^19-bit bitmaps, 64 KB each)
 #define BS_BM_WORDS (2u << (BS_FB - 5))           // both bitmaps, 32-bit words
-#define BS_SMEM ((size_t)BS_BM_WORDS * 4 + (size_t)BS_STAGES * BS_TILE * sizeof(BsRec))
+#define BS_SMEM ((size_t)BS_BM_WORDS * 4 + (size_t)BS_STAGES * BS_TILE * sizeof(BsRec) + BS_WARPS * sizeof(BsWarp))
 
 struct BsRec {
     ulonglong2 x;      // X_k
@@ -522,6 +525,17 @@ struct BsRec {
     uint32_t sb;       // strings [sb, se) of group k
     uint32_t se;       // bit 31: same-spin quad (two-of-four test)
     uint32_t pad;
+};
+
+// per-warp shared state of k_eloc_bs (in the dynamic shared memory, after the tile ring)
+struct __align__(16) BsWarp {
+    ulonglong2 rx[BS_P * 32];   // the warp's rows: key
+    uint4 rh[BS_P * 32];        //   h(x) lo, hi, f_alpha(x), f_beta(x)
+    double2 rl[BS_P * 32];      //   log psi(x)
+    double qh[32];              // hits of one round: H_xx', psi(x')/psi-hat factor, row
+    double2 qp[32];
+    uint32_t pl[BS_P][132];     // bit planes of the warp's rows (+ zero, ones)
+    int32_t qr[32];
 };
 
 // Algorithm 2's lookup of x' (the probe above) with the common case -- an absent key
@@ -559,27 +573,25 @@ __global__ void __launch_bounds__(BS_WARPS * 32, 1) k_eloc_bs(HamView H, const B
                                                               const ulonglong2 *rows, const double2 *row_lp,
                                                               int64_t n_rows, double2 *out,
                                                               unsigned long long *stats, ChunkSink cs) {
+    constexpr int NP = BS_P;                        // 32-row blocks per warp (one group tile feeds 32 NP rows)
     extern __shared__ __align__(128) unsigned char bs_smem[];
     uint32_t *s_bm = reinterpret_cast<uint32_t *>(bs_smem);                          // [2][2^BS_FB / 32]
     BsRec *tile = reinterpret_cast<BsRec *>(bs_smem + (size_t)BS_BM_WORDS * 4);    // [BS_STAGES][BS_TILE]
-    __shared__ uint32_t s_pl[BS_WARPS][130];        // bit planes of the warp's 32 rows (+ zero, ones)
-    __shared__ ulonglong2 s_rx[BS_WARPS][32];       // the warp's rows: key
-    __shared__ uint4 s_rh[BS_WARPS][32];            //   h(x) lo, hi, f_alpha(x), f_beta(x)
-    __shared__ double2 s_rl[BS_WARPS][32];          //   log psi(x)
-    __shared__ double s_qh[BS_WARPS][32];           // hits of one round: H_xx', psi-hat ratio, row
-    __shared__ double2 s_qp[BS_WARPS][32];
-    __shared__ int32_t s_qr[BS_WARPS][32];
+    BsWarp *s_w = reinterpret_cast<BsWarp *>(bs_smem + (size_t)BS_BM_WORDS * 4 +
+                                             (size_t)BS_STAGES * BS_TILE * sizeof(BsRec));   // [BS_WARPS]
     __shared__ __align__(8) unsigned long long full[BS_STAGES];
     __shared__ unsigned s_done[BS_STAGES];          // warps done with the stage's current tile
     const int kWarps = blockDim.x / 32;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned FULL = 0xffffffffu;
+    BsWarp &W = s_w[wid];
     const double s = dkey_inv(*T.shift_key);
     const int64_t K = H.K;
     const int64_t n_tiles = (K + BS_TILE - 1) / BS_TILE;
     u64 c_pairs = 0, c_sec = 0, c_hit = 0, c_str = 0;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t first = (int64_t)blockIdx.x * blockDim.x;
+    const int64_t per_cta = (int64_t)blockDim.x * NP;
+    const int64_t stride = (int64_t)gridDim.x * per_cta;
+    const int64_t first = (int64_t)blockIdx.x * per_cta;
     const int64_t n_blocks = first < n_rows ? (n_rows - first + stride - 1) / stride : 0;
     const int64_t q_end = n_blocks * n_tiles;
     auto issue = [&](int64_t q) {
@@ -598,70 +610,85 @@ __global__ void __launch_bounds__(BS_WARPS * 32, 1) k_eloc_bs(HamView H, const B
     }
     for (uint32_t i = threadIdx.x; i < BS_BM_WORDS / 4; i += blockDim.x)
         reinterpret_cast<uint4 *>(s_bm)[i] = __ldg(reinterpret_cast<const uint4 *>(bm) + i);
-    if (lane == 0) {
-        s_pl[wid][128] = 0u;
-        s_pl[wid][129] = ~0u;
+    if (lane < NP) {
+        W.pl[lane][128] = 0u;
+        W.pl[lane][129] = ~0u;
     }
     __syncthreads();
     if (threadIdx.x == 0)
         for (int64_t q = 0; q < BS_STAGES && q < q_end; ++q) issue(q);
     const uint32_t *bmA = s_bm, *bmB = s_bm + BS_BM_WORDS / 2;
-    uint32_t *pl = s_pl[wid];
     int64_t q = 0;
     for (int64_t blk = 0; blk < n_blocks; ++blk) {
-        const int64_t r = first + blk * stride + threadIdx.x;
-        u64 x0 = 0, x1 = 0;
-        double2 lx = make_double2(-INFINITY, 0.0);
-        if (r < n_rows) {
-            if (rows) {
-                const ulonglong2 k = rows[r];
-                x0 = k.x;
-                x1 = k.y;
-                lx = row_lp[r];
-            } else {
-                const ulonglong2 k = T.keys[row_begin + r];
-                x0 = k.x;
-                x1 = k.y;
-                lx = T.logpsi[row_begin + r];
-            }
-        }
-        const bool live = lx.x > -INFINITY;      // psi(x) = 0 (reading R10) or past the end: no pairs
-        const uint32_t live_m = __ballot_sync(FULL, live);
+        const int64_t r0 = first + blk * stride + (int64_t)wid * 32 * NP;   // the warp's NP x 32 rows
+        double2 lx[NP];
+        uint32_t live_m[NP];
         __syncwarp();
-        {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const int64_t r = r0 + 32 * p + lane;
+            u64 x0 = 0, x1 = 0;
+            lx[p] = make_double2(-INFINITY, 0.0);
+            if (r < n_rows) {
+                if (rows) {
+                    const ulonglong2 k = rows[r];
+                    x0 = k.x;
+                    x1 = k.y;
+                    lx[p] = row_lp[r];
+                } else {
+                    const ulonglong2 k = T.keys[row_begin + r];
+                    x0 = k.x;
+                    x1 = k.y;
+                    lx[p] = T.logpsi[row_begin + r];
+                }
+            }
+            const bool live = lx[p].x > -INFINITY;   // psi(x) = 0 (reading R10) or past the end: no pairs
+            live_m[p] = __ballot_sync(FULL, live);
             const u64 hx = live ? hash128(x0, x1) : 0;
             const uint32_t fa = live ? ffilt(x0 & ALPHA_MASK, 0) ^ ffilt(x1 & ALPHA_MASK, 64) : 0;
             const uint32_t fb = live ? ffilt(x0 & BETA_MASK, 0) ^ ffilt(x1 & BETA_MASK, 64) : 0;
-            s_rx[wid][lane] = make_ulonglong2(x0, x1);
-            s_rh[wid][lane] = make_uint4((uint32_t)hx, (uint32_t)(hx >> 32), fa, fb);
-            s_rl[wid][lane] = lx;
+            W.rx[32 * p + lane] = make_ulonglong2(x0, x1);
+            W.rh[32 * p + lane] = make_uint4((uint32_t)hx, (uint32_t)(hx >> 32), fa, fb);
+            W.rl[32 * p + lane] = lx[p];
+            for (int b = 0; b < 128; ++b) {          // bit planes of the block's rows
+                const uint32_t v = __ballot_sync(FULL, ((b < 64 ? x0 >> b : x1 >> (b - 64)) & 1ULL) != 0);
+                if (lane == (b & 31)) W.pl[p][b] = v;
+            }
         }
-        for (int p = 0; p < 128; ++p) {          // bit planes of the warp's rows
-            const uint32_t v = __ballot_sync(FULL, ((p < 64 ? x0 >> p : x1 >> (p - 64)) & 1ULL) != 0);
-            if (lane == (p & 31)) pl[p] = v;
-        }
+        uint32_t any_live = 0;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) any_live |= live_m[p];
         __syncwarp();
-        double ar = 0.0, ai = 0.0;
+        double ar[NP], ai[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) ar[p] = ai[p] = 0.0;
         for (int64_t t = 0; t < n_tiles; ++t, ++q) {
             const int st = (int)(q % BS_STAGES);
             const unsigned ph = (unsigned)((q / BS_STAGES) & 1);
             mbar_wait(&full[st], ph);
             const BsRec *tl = tile + st * BS_TILE;
-            const int gn = live_m ? (int)min((int64_t)BS_TILE, K - t * BS_TILE) : 0;
+            const int gn = any_live ? (int)min((int64_t)BS_TILE, K - t * BS_TILE) : 0;
             for (int g0 = 0; g0 < gn; g0 += 32) {
-                // lane = group g0 + lane: the 32-row in-sector mask
-                uint32_t m = 0;
+                // lane = group g0 + lane: the in-sector masks of the NP row blocks
+                uint32_t m[NP];
+#pragma unroll
+                for (int p = 0; p < NP; ++p) m[p] = 0;
                 if (g0 + lane < gn) {
                     const uint32_t pos = tl[g0 + lane].pos, se = tl[g0 + lane].se;
-                    const uint32_t P0 = pl[pos & 0xff], P1 = pl[(pos >> 8) & 0xff];
-                    const uint32_t P2 = pl[(pos >> 16) & 0xff], P3 = pl[pos >> 24];
-                    const uint32_t s1 = P0 ^ P1, s2 = P2 ^ P3;
-                    if (se >> 31) m = (s1 & s2) | (((P0 & P1) ^ (P2 & P3)) & ~(s1 | s2));
-                    else m = s1 & s2;
-                    m &= live_m;
+                    const uint32_t i0 = pos & 0xff, i1 = (pos >> 8) & 0xff, i2 = (pos >> 16) & 0xff, i3 = pos >> 24;
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+                        const uint32_t *pl = W.pl[p];
+                        const uint32_t P0 = pl[i0], P1 = pl[i1], P2 = pl[i2], P3 = pl[i3];
+                        const uint32_t s1 = P0 ^ P1, s2 = P2 ^ P3;
+                        m[p] = ((se >> 31) ? (s1 & s2) | (((P0 & P1) ^ (P2 & P3)) & ~(s1 | s2)) : (s1 & s2)) &
+                               live_m[p];
+                    }
                 }
-                // the in-sector (group, row) pairs, flattened over the warp in (group, row) order
-                const int cnt = __popc(m);
+                // the in-sector (group, row) pairs, flattened over the warp in (group, block, row) order
+                int cnt = 0;
+#pragma unroll
+                for (int p = 0; p < NP; ++p) cnt += __popc(m[p]);
                 int incl = cnt;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -680,13 +707,27 @@ __global__ void __launch_bounds__(BS_WARPS * 32, 1) k_eloc_bs(HamView H, const B
                         const int ex = __shfl_sync(FULL, excl, cnd & 31);
                         if (cnd < 32 && ex <= f) lo = cnd;
                     }
-                    const uint32_t mo = __shfl_sync(FULL, m, lo);
+                    uint32_t mo[NP];
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) mo[p] = __shfl_sync(FULL, m[p], lo);
                     const int exo = __shfl_sync(FULL, excl, lo);
                     int64_t idx = -1;
                     int row = 0;
                     if (f < total) {
-                        int k = f - exo;                 // row = the k-th set bit of mo
-                        uint32_t v = mo;
+                        int k = f - exo;                 // row = the k-th set bit of mo[0] | mo[1] << 32 | ...
+                        uint32_t v = mo[NP - 1];
+                        int base = 32 * (NP - 1);
+#pragma unroll
+                        for (int p = 0; p < NP - 1; ++p) {
+                            const int c = __popc(mo[p]);
+                            if (k < c) {
+                                v = mo[p];
+                                base = 32 * p;
+                                break;
+                            }
+                            k -= c;
+                        }
+                        row = base;
 #pragma unroll
                         for (int sh = 16; sh; sh >>= 1) {
                             const int c = __popc(v & ((1u << sh) - 1u));
@@ -696,10 +737,10 @@ __global__ void __launch_bounds__(BS_WARPS * 32, 1) k_eloc_bs(HamView H, const B
                                 row += sh;
                             }
                         }
-                        const uint4 rh = s_rh[wid][row];
+                        const uint4 rh = W.rh[row];
                         const BsRec &G = tl[g0 + lo];
                         if (bm_test(bmA, rh.z ^ G.fa) && bm_test(bmB, rh.w ^ G.fb)) {
-                            const ulonglong2 xr = s_rx[wid][row];
+                            const ulonglong2 xr = W.rx[row];
                             const ulonglong2 X = G.x;
                             const u64 hxr = (u64)rh.x | ((u64)rh.y << 32);
                             idx = probe_fast(T, hxr ^ G.hx, xr.x ^ X.x, xr.y ^ X.y);
@@ -707,9 +748,9 @@ __global__ void __launch_bounds__(BS_WARPS * 32, 1) k_eloc_bs(HamView H, const B
                     }
                     const unsigned hm = __ballot_sync(FULL, idx >= 0);
                     if (hm) {                            // rare: ~0.4 hits per 32 x 32 pairs at C5
-                        if (idx >= 0) {                  // H_xx' (strings in order) and psi(x')/psi-hat
+                        if (idx >= 0) {                  // H_xx': the group's strings in order
                             const BsRec &G = tl[g0 + lo];
-                            const ulonglong2 xr = s_rx[wid][row];
+                            const ulonglong2 xr = W.rx[row];
                             const uint32_t b = G.sb, e = G.se & 0x7FFFFFFFu;
                             double hv = 0.0;
                             for (uint32_t i = b; i < e; ++i) {
@@ -718,31 +759,36 @@ __global__ void __launch_bounds__(BS_WARPS * 32, 1) k_eloc_bs(HamView H, const B
                                 hv += flip_sign(__ldg(H.td + i), par);
                             }
                             c_str += e - b;
-                            const double2 lr = s_rl[wid][row];
+                            const double2 lr = W.rl[row];
                             double2 ps;
                             if (!((lr.x - s) < -600.0)) {
                                 ps = __ldg(T.psi_hat + idx);
-                            } else {
-                                const double2 l = T.logpsi[idx];
-                                const double mm = exp(l.x - lr.x);
+                            } else {                     // reading R11
+                                const double2 l2 = T.logpsi[idx];
+                                const double mm = exp(l2.x - lr.x);
                                 double sn, cs2;
-                                sincos(l.y - lr.y, &sn, &cs2);
+                                sincos(l2.y - lr.y, &sn, &cs2);
                                 ps = make_double2(mm * cs2, mm * sn);
                             }
-                            s_qh[wid][lane] = hv;
-                            s_qp[wid][lane] = ps;
-                            s_qr[wid][lane] = row;
+                            W.qh[lane] = hv;
+                            W.qp[lane] = ps;
+                            W.qr[lane] = row;
                         }
                         __syncwarp();
                         unsigned h2 = hm;                // each row adds its hits in (group) order
                         while (h2) {
                             const int l = __ffs(h2) - 1;
                             h2 &= h2 - 1;
-                            if (s_qr[wid][l] == lane) {
-                                const double hv = s_qh[wid][l];
-                                const double2 ps = s_qp[wid][l];
-                                ar = fma(hv, ps.x, ar);
-                                ai = fma(hv, ps.y, ai);
+                            const int rw = W.qr[l];
+                            if ((rw & 31) == lane) {
+                                const double hv = W.qh[l];
+                                const double2 ps = W.qp[l];
+#pragma unroll
+                                for (int p = 0; p < NP; ++p) {
+                                    if ((rw >> 5) != p) continue;
+                                    ar[p] = fma(hv, ps.x, ar[p]);
+                                    ai[p] = fma(hv, ps.y, ai[p]);
+                                }
                                 ++c_hit;
                             }
                         }
@@ -762,25 +808,29 @@ __global__ void __launch_bounds__(BS_WARPS * 32, 1) k_eloc_bs(HamView H, const B
                 }
             }
         }
-        if (r < n_rows) {
-            double2 e;
-            if (!live) {
-                e = make_double2(NAN, NAN);
-            } else if ((lx.x - s) < -600.0) {
-                e = make_double2(ar, ai);
-            } else {
-                // E = acc / psi_hat(x) = acc * exp(-(logpsi(x) - s))
-                const double mm = exp(-(lx.x - s));
-                double sn, cs2;
-                sincos(-lx.y, &sn, &cs2);
-                const double ir = mm * cs2, ii = mm * sn;
-                e = make_double2(ar * ir - ai * ii, ar * ii + ai * ir);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const int64_t r = r0 + 32 * p + lane;
+            if (r < n_rows) {
+                const bool live = lx[p].x > -INFINITY;
+                double2 e;
+                if (!live) {
+                    e = make_double2(NAN, NAN);
+                } else if ((lx[p].x - s) < -600.0) {
+                    e = make_double2(ar[p], ai[p]);
+                } else {
+                    // E = acc / psi_hat(x) = acc * exp(-(logpsi(x) - s))
+                    const double mm = exp(-(lx[p].x - s));
+                    double sn, cs2;
+                    sincos(-lx[p].y, &sn, &cs2);
+                    const double ir = mm * cs2, ii = mm * sn;
+                    e = make_double2(ar[p] * ir - ai[p] * ii, ar[p] * ii + ai[p] * ir);
+                }
+                if (live) c_pairs += (u64)K;
+                out[r] = e;
+                chunk_done_thread(cs, out, r, n_rows);
             }
-            if (live) c_pairs += (u64)K;
-            out[r] = e;
-            chunk_done_thread(cs, out, r, n_rows);
         }
-        __syncwarp();                                // row arrays reused by the next block
     }
     if (stats) {
         for (int o = 16; o; o >>= 1) {
@@ -1090,9 +1140,9 @@ int nnqs_launch_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const 
     if (lk == NNQS_LIT_AUTO && t->mode == 0 && cons && h->dev.gbs && t->bsbm) {   // bit-sliced (k_eloc_bs)
         cudaFuncSetAttribute(k_eloc_bs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BS_SMEM);
         // one CTA per SM, 32 rows per warp; fewer warps per CTA when the rows would not fill 148 CTAs
-        const int64_t warps_needed = (n_rows + 31) / 32;
+        const int64_t warps_needed = (n_rows + 32 * BS_P - 1) / (32 * BS_P);
         const int64_t per = std::min<int64_t>(BS_WARPS, std::max<int64_t>(1, (warps_needed + 147) / 148)) * 32;
-        const int gl = (int)std::min<int64_t>((n_rows + per - 1) / per, 148);
+        const int gl = (int)std::min<int64_t>((n_rows + per * BS_P - 1) / (per * BS_P), 148);
         k_eloc_bs<<<gl, (unsigned)per, BS_SMEM, st>>>(H, (const BsRec *)h->dev.gbs, T, t->bsbm, row_begin, r, rl,
                                                        n_rows, o, s, cs);
         return cuda_check(cudaGetLastError(), "local energy launch");
