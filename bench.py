@@ -471,9 +471,10 @@ def run_ours(args):
         return tab, en
 
     clk = ClockSampler(local).__enter__()   # sampling from before the warm-up: no thread start in the timed region
-    for _ in range(args.warmup):       # the same work as a timed step (L2 flush included)
+    for _ in range(args.warmup):       # the same work and host pattern as a timed step (L2 flush, per-step sync)
         flush.fill_(1)
         tab, en = step(keys_d, lp_d, cnt_d, False)
+        torch.cuda.current_stream().synchronize()
         tab.close()
     torch.cuda.synchronize()
 
