@@ -408,6 +408,9 @@ def run_ours(args):
         if os.environ.get("NNQS_BENCH_SHARED_GPU"):
             dist.init_process_group("gloo")
         else:
+            # NCCL's own log (stderr) shows the communicator (comm_nranks, NVLS / P2P transport)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
     name = args.config
     c, mol, st = workload(name)

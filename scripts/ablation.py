@@ -2,11 +2,15 @@
 local-energy time for one call over every row of a sample table, for
   cpu_oracle  -- the oracle (plain term-by-term Eq. 9, sample-aware with a
                  bisection lookup, all host cores): the CPU reference point
-  gpu_literal -- Algorithm 2 on the GPU: every (row, flip group) pair, sector
-                 test, GF(2)-hash lookup of x' (sample-aware + fused + LUT + GPU)
+  gpu_literal_plain / _staged / _bitsliced -- Algorithm 2 on the GPU: every (row,
+                 flip group) pair, sector test, GF(2)-hash lookup of x' (sample-aware +
+                 fused + LUT + GPU): one row per thread reading the group table from
+                 global memory / group tiles staged in shared memory by bulk copies /
+                 32 rows x 32 groups per bit-sliced sector test (bit-identical results)
   gpu_structured -- the alpha/beta-factorised enumeration of the same pairs
 Workloads: C4 (N2-shaped, N = 20, the whole 14,400-entry sector as the table;
-the paper's C2 run is N = 20 with N_u = 10,553) and C3 (H2O-shaped, N = 14).
+the paper's C2 run is N = 20 with N_u = 10,553), C3 (H2O-shaped, N = 14) and the
+first 2048 rows of C5 (N = 120, 10^6-entry table; the oracle on those rows only).
 Writes one JSON object to stdout.  Dev/evidence tool, run on the GPU box.
 """
 import json
@@ -28,6 +32,7 @@ from synth import configs as C  # noqa: E402
 
 def gpu_time(ham, tab, n, algo, reps=20):
     nnqs.nnqs_table_set_algorithm(tab, algo)
+    reps = reps if n * ham.info()["n_groups"] < 10 ** 10 else 2
     out = torch.empty((n, 2), dtype=torch.float64, device="cuda")
     for _ in range(3):
         nnqs.nnqs_local_energy(ham, tab, 0, n_rows=n, eloc_out=out)
@@ -45,27 +50,34 @@ def gpu_time(ham, tab, n, algo, reps=20):
 def main():
     res = {"what": "local energy over every table row, one call", "device": torch.cuda.get_device_name(0),
            "oracle_threads": R.num_threads(), "workloads": []}
-    for c in (3, 4):
+    for c in (3, 4, 5):
         m = C.molecule(c)
-        st = C.sample_table(c, "full")
-        n = len(st.keys)
+        st = C.sample_table(c, "full") if c < 5 else C.sample_table(5)
+        n = len(st.keys) if c < 5 else 2048
         ham = nnqs.nnqs_ham_compress(m.h1, m.h2, m.n_qubits, m.e_core, device=0)
-        tab = nnqs.nnqs_table_prepare(ham, 0, torch.from_numpy(st.keys.view(np.int64)).cuda(),
-                                      torch.from_numpy(st.logpsi).cuda())
+        keys_d = torch.from_numpy(st.keys.view(np.int64)).cuda()
+        lp_d = torch.from_numpy(st.logpsi).cuda()
         t0 = time.perf_counter()
-        ref = R.eloc(m.h1, m.h2, m.e_core, st.keys, st.logpsi, keys=st.keys, logpsi=st.logpsi)
+        ref = R.eloc(m.h1, m.h2, m.e_core, st.keys[:n], st.logpsi[:n], keys=st.keys, logpsi=st.logpsi)
         t_cpu = time.perf_counter() - t0
-        t_lit, el_lit = gpu_time(ham, tab, n, nnqs.ALGO_LITERAL)
-        t_str, el_str = gpu_time(ham, tab, n, nnqs.ALGO_AUTO)
+        secs, els = {"cpu_oracle": t_cpu}, {}
+        for name, lk in (("gpu_literal_plain", 2), ("gpu_literal_staged", 1), ("gpu_literal_bitsliced", 0)):
+            tab = nnqs.nnqs_table_prepare(ham, 0, keys_d, lp_d, literal_kernel=lk)
+            secs[name], els[name] = gpu_time(ham, tab, n, nnqs.ALGO_LITERAL)
+            tab.close()
+        tab = nnqs.nnqs_table_prepare(ham, 0, keys_d, lp_d)
+        secs["gpu_structured"], els["gpu_structured"] = gpu_time(ham, tab, n, nnqs.ALGO_AUTO)
+        tab.close()
         scale = np.max(np.abs(ref))
         res["workloads"].append({
-            "config": f"C{c}: {m.name}, N={m.n_qubits}, N_u={n}, K'={ham.info()['n_groups']}, "
+            "config": f"C{c}: {m.name}, N={m.n_qubits}, N_u={len(st.keys)}, rows={n}, K'={ham.info()['n_groups']}, "
                       f"N_h={ham.info()['n_terms']}",
-            "seconds": {"cpu_oracle": t_cpu, "gpu_literal": t_lit, "gpu_structured": t_str},
-            "speedup_vs_cpu_oracle": {"gpu_literal": t_cpu / t_lit, "gpu_structured": t_cpu / t_str},
+            "seconds": secs,
+            "speedup_vs_cpu_oracle": {k: t_cpu / v for k, v in secs.items() if k != "cpu_oracle"},
+            "literal_kernels_bit_identical": all(els[k].tobytes() == els["gpu_literal_plain"].tobytes()
+                                                 for k in els if k.startswith("gpu_literal")),
             "max_abs_diff_vs_oracle_over_max_abs": {
-                "gpu_literal": float(np.max(np.abs(el_lit[:, 0] + 1j * el_lit[:, 1] - ref)) / scale),
-                "gpu_structured": float(np.max(np.abs(el_str[:, 0] + 1j * el_str[:, 1] - ref)) / scale)},
+                k: float(np.max(np.abs(v[:, 0] + 1j * v[:, 1] - ref)) / scale) for k, v in els.items()},
         })
     print(json.dumps(res))
 

@@ -1,7 +1,7 @@
 """Workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
 the whole C-ABI path on C2-C4 and a 4096-row C5 slice -- table prepare (order
 check, psi_hat, hash, alpha/beta index, deletion multimap), both local-energy
-algorithms, the fused Eq. (6) chunk partials, the reduce, the Eq. (7) weights
+algorithms (the literal loop in its bit-sliced and staged kernels), the fused Eq. (6) chunk partials, the reduce, the Eq. (7) weights
 and the production-path hit log.  Exits non-zero on any API error; the
 sanitizer's own exit code reports device errors.
 
@@ -41,10 +41,17 @@ def run(c, n_rows=None, variant="full", **opt):
     m1 = nnqs.nnqs_energy_combine(part, 1)
     nnqs.nnqs_grad_weights(el, cnt, m1)
     nnqs.nnqs_coupled_debug_rows(ham, tab, r0, min(n, 64), max_pairs=1 << 20)
-    if c < 5:
+    if c < 5:   # literal loop: bit-sliced (default) and staged kernels
         nnqs.nnqs_table_set_algorithm(tab, nnqs.ALGO_LITERAL)
         nnqs.nnqs_local_energy(ham, tab, r0, n_rows=n, counts=cnt, partials_out=part)
         nnqs.nnqs_local_energy(ham, tab, rows=t(st.keys[:64], dev), row_logpsi=t(st.logpsi[:64], dev))
+        tl = nnqs.nnqs_table_prepare(ham, 0, t(st.keys, dev), t(st.logpsi, dev), algorithm=nnqs.ALGO_LITERAL,
+                                     literal_kernel=1)
+        nnqs.nnqs_local_energy(ham, tl, r0, n_rows=n)
+        tl.close()
+    else:       # the bit-sliced literal kernel on 40 explicit C5 rows (2.06M groups each)
+        nnqs.nnqs_table_set_algorithm(tab, nnqs.ALGO_LITERAL)
+        nnqs.nnqs_local_energy(ham, tab, rows=t(st.keys[:40], dev), row_logpsi=t(st.logpsi[:40], dev))
     nnqs.nnqs_chunk_work(tab, with_floor=True)
     torch.cuda.synchronize()
     tab.close()
