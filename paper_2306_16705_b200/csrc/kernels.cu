@@ -494,8 +494,8 @@ __global__ void __launch_bounds__(LIT_THREADS, 1) k_eloc_lit(HamView H, const Li
 //   a pair per spin     (P_i ^ P_j) & (P_k ^ P_l)
 //   a same-spin quad    exactly two of P_i, P_j, P_k, P_l set.
 // The in-sector (group, row) pairs of the 32 x 32 block (~16 % at C5) are then
-// flattened over the warp, 32 at a time in (group, row) order, so every lane has
-// a pair and its lookup in flight: a per-spin string filter (f_alpha(x'),
+// queued in shared memory in (group, row) order and taken 32 at a time, so every
+// lane has a pair and its lookup in flight: a per-spin string filter (f_alpha(x'),
 // f_beta(x') in shared-memory bitmaps of the table's alpha and beta strings --
 // GF(2)-linear, f(x ^ X) = f(x) ^ f(X); no false negatives), then the hash
 // probe of Algorithm 2's lookup, then, on a hit, the string sum.  Each row's
@@ -508,7 +508,10 @@ __global__ void __launch_bounds__(LIT_THREADS, 1) k_eloc_lit(HamView H, const Li
 #define BS_TILE 256
 #endif
 #ifndef BS_STAGES
-#define BS_STAGES 4
+#define BS_STAGES 3
+#endif
+#ifndef BS_FQ
+#define BS_FQ 512                                 // pair-queue entries per warp (a batch has <= 32 x 32 BS_P)
 #endif
 #ifndef BS_P
 #define BS_P 1                                    // 32-row blocks per warp (2 and 4 measured slower)
@@ -536,6 +539,7 @@ struct __align__(16) BsWarp {
     double2 qp[32];
     uint32_t pl[BS_P][132];     // bit planes of the warp's rows (+ zero, ones)
     int32_t qr[32];
+    uint16_t fq[BS_FQ];         // in-sector pairs of a batch in (group, row) order: group | row << 8
 };
 
 // Algorithm 2's lookup of x' (the probe above) with the common case -- an absent key
@@ -698,109 +702,96 @@ __global__ void __launch_bounds__(BS_WARPS * 32, 1) k_eloc_bs(HamView H, const B
                 const int excl = incl - cnt;
                 const int total = __shfl_sync(FULL, incl, 31);
                 c_sec += cnt;
-                for (int f0 = 0; f0 < total; f0 += 32) {
-                    const int f = f0 + lane;
-                    int lo = 0;                          // owner: the last lane with excl <= f
+                for (int base = 0; base < total; base += BS_FQ) {
+                    {   // this lane's pairs (ascending row) at positions excl.. of the (group, row) order
+                        int j = excl;
 #pragma unroll
-                    for (int sp = 16; sp; sp >>= 1) {
-                        const int cnd = lo + sp;
-                        const int ex = __shfl_sync(FULL, excl, cnd & 31);
-                        if (cnd < 32 && ex <= f) lo = cnd;
-                    }
-                    uint32_t mo[NP];
-#pragma unroll
-                    for (int p = 0; p < NP; ++p) mo[p] = __shfl_sync(FULL, m[p], lo);
-                    const int exo = __shfl_sync(FULL, excl, lo);
-                    int64_t idx = -1;
-                    int row = 0;
-                    if (f < total) {
-                        int k = f - exo;                 // row = the k-th set bit of mo[0] | mo[1] << 32 | ...
-                        uint32_t v = mo[NP - 1];
-                        int base = 32 * (NP - 1);
-#pragma unroll
-                        for (int p = 0; p < NP - 1; ++p) {
-                            const int c = __popc(mo[p]);
-                            if (k < c) {
-                                v = mo[p];
-                                base = 32 * p;
-                                break;
-                            }
-                            k -= c;
-                        }
-                        row = base;
-#pragma unroll
-                        for (int sh = 16; sh; sh >>= 1) {
-                            const int c = __popc(v & ((1u << sh) - 1u));
-                            if (k >= c) {
-                                k -= c;
-                                v >>= sh;
-                                row += sh;
+                        for (int p = 0; p < NP; ++p) {
+                            uint32_t v = m[p];
+                            while (v) {
+                                const int r = __ffs(v) - 1;
+                                v &= v - 1;
+                                if (j >= base && j < base + BS_FQ) W.fq[j - base] = (uint16_t)(lane | ((32 * p + r) << 8));
+                                ++j;
                             }
                         }
-                        const uint4 rh = W.rh[row];
-                        const BsRec &G = tl[g0 + lo];
-                        if (bm_test(bmA, rh.z ^ G.fa) && bm_test(bmB, rh.w ^ G.fb)) {
-                            const ulonglong2 xr = W.rx[row];
-                            const ulonglong2 X = G.x;
-                            const u64 hxr = (u64)rh.x | ((u64)rh.y << 32);
-                            idx = probe_fast(T, hxr ^ G.hx, xr.x ^ X.x, xr.y ^ X.y);
-                        }
                     }
-                    const unsigned hm = __ballot_sync(FULL, idx >= 0);
-                    if (hm) {                            // rare: ~0.4 hits per 32 x 32 pairs at C5
-                        if (idx >= 0) {                  // H_xx': the group's strings in order
+                    __syncwarp();
+                    const int lim = min(total, base + BS_FQ);
+                    for (int f0 = base; f0 < lim; f0 += 32) {
+                        const int f = f0 + lane;
+                        int64_t idx = -1;
+                        int row = 0, lo = 0;
+                        if (f < lim) {
+                            const uint32_t e = W.fq[f - base];
+                            lo = (int)(e & 0xff);
+                            row = (int)(e >> 8);
+                            const uint4 rh = W.rh[row];
                             const BsRec &G = tl[g0 + lo];
-                            const ulonglong2 xr = W.rx[row];
-                            const uint32_t b = G.sb, e = G.se & 0x7FFFFFFFu;
-                            double hv = 0.0;
-                            for (uint32_t i = b; i < e; ++i) {
-                                const ulonglong2 Z = __ldg(H.tz + i);
-                                const int par = (__popcll(xr.x & Z.x) + __popcll(xr.y & Z.y)) & 1;
-                                hv += flip_sign(__ldg(H.td + i), par);
+                            if (bm_test(bmA, rh.z ^ G.fa) && bm_test(bmB, rh.w ^ G.fb)) {
+                                const ulonglong2 xr = W.rx[row];
+                                const ulonglong2 X = G.x;
+                                const u64 hxr = (u64)rh.x | ((u64)rh.y << 32);
+                                idx = probe_fast(T, hxr ^ G.hx, xr.x ^ X.x, xr.y ^ X.y);
                             }
-                            c_str += e - b;
-                            const double2 lr = W.rl[row];
-                            double2 ps;
-                            if (!((lr.x - s) < -600.0)) {
-                                ps = __ldg(T.psi_hat + idx);
-                            } else {                     // reading R11
-                                const double2 l2 = T.logpsi[idx];
-                                const double mm = exp(l2.x - lr.x);
-                                double sn, cs2;
-                                sincos(l2.y - lr.y, &sn, &cs2);
-                                ps = make_double2(mm * cs2, mm * sn);
-                            }
-                            W.qh[lane] = hv;
-                            W.qp[lane] = ps;
-                            W.qr[lane] = row;
                         }
-                        __syncwarp();
-                        unsigned h2 = hm;                // each row adds its hits in (group) order
-                        while (h2) {
-                            const int l = __ffs(h2) - 1;
-                            h2 &= h2 - 1;
-                            const int rw = W.qr[l];
-                            if ((rw & 31) == lane) {
-                                const double hv = W.qh[l];
-                                const double2 ps = W.qp[l];
-#pragma unroll
-                                for (int p = 0; p < NP; ++p) {
-                                    if ((rw >> 5) != p) continue;
-                                    ar[p] = fma(hv, ps.x, ar[p]);
-                                    ai[p] = fma(hv, ps.y, ai[p]);
+                        const unsigned hm = __ballot_sync(FULL, idx >= 0);
+                        if (hm) {                            // rare: ~0.4 hits per 32 x 32 pairs at C5
+                            if (idx >= 0) {                  // H_xx': the group's strings in order
+                                const BsRec &G = tl[g0 + lo];
+                                const ulonglong2 xr = W.rx[row];
+                                const uint32_t b = G.sb, e = G.se & 0x7FFFFFFFu;
+                                double hv = 0.0;
+                                for (uint32_t i = b; i < e; ++i) {
+                                    const ulonglong2 Z = __ldg(H.tz + i);
+                                    const int par = (__popcll(xr.x & Z.x) + __popcll(xr.y & Z.y)) & 1;
+                                    hv += flip_sign(__ldg(H.td + i), par);
                                 }
-                                ++c_hit;
+                                c_str += e - b;
+                                const double2 lr = W.rl[row];
+                                double2 ps;
+                                if (!((lr.x - s) < -600.0)) {
+                                    ps = __ldg(T.psi_hat + idx);
+                                } else {                     // reading R11
+                                    const double2 l2 = T.logpsi[idx];
+                                    const double mm = exp(l2.x - lr.x);
+                                    double sn, cs2;
+                                    sincos(l2.y - lr.y, &sn, &cs2);
+                                    ps = make_double2(mm * cs2, mm * sn);
+                                }
+                                W.qh[lane] = hv;
+                                W.qp[lane] = ps;
+                                W.qr[lane] = row;
                             }
+                            __syncwarp();
+                            unsigned h2 = hm;                // each row adds its hits in (group) order
+                            while (h2) {
+                                const int l = __ffs(h2) - 1;
+                                h2 &= h2 - 1;
+                                const int rw = W.qr[l];
+                                if ((rw & 31) == lane) {
+                                    const double hv = W.qh[l];
+                                    const double2 ps = W.qp[l];
+    #pragma unroll
+                                    for (int p = 0; p < NP; ++p) {
+                                        if ((rw >> 5) != p) continue;
+                                        ar[p] = fma(hv, ps.x, ar[p]);
+                                        ai[p] = fma(hv, ps.y, ai[p]);
+                                    }
+                                    ++c_hit;
+                                }
+                            }
+                            __syncwarp();
                         }
-                        __syncwarp();
                     }
+                    __syncwarp();                        // the queue is refilled by the next pass / batch
                 }
             }
             __syncwarp();
             if (lane == 0) {                         // the last warp done with the tile refills the stage
                 __threadfence_block();
                 if (atomicAdd(&s_done[st], 1u) == (unsigned)kWarps - 1) {
-                    s_done[st] = 0;
+                    atomicExch(&s_done[st], 0u);
                     if (q + BS_STAGES < q_end) {
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                         issue(q + BS_STAGES);
