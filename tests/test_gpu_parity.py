@@ -441,6 +441,11 @@ def test_c5_fixture_every_row(nnqs, dev, c5):
         var = float(z["var"])
         assert abs(m2[0] - var) <= TOL * var + 2 * TOL * np.sqrt(var) * float(z["max_abs"])
         assert m1[2] == float(z["W"])
+    # the literal Algorithm 2 loop (bit-sliced kernel) over every row too
+    lit = nnqs.nnqs_table_prepare(ham, 0, _t(st.keys, dev), _t(st.logpsi, dev), algorithm=nnqs.ALGO_LITERAL)
+    got_l = _c(nnqs.nnqs_local_energy(ham, lit, 0, n_rows=n))
+    lit.close()
+    _assert_close(got_l[have], ref, z["scale"][have], f"C5 fixture, literal loop ({int(have.sum())} rows)")
 
 
 # ---------------------------------------------------- Pauli-level semantics
