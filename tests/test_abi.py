@@ -65,3 +65,18 @@ def test_host_only_errors_without_gpu(lib_path):
     with pytest.raises(nnqs.NNQSError) as e:   # Y0 alone: odd Y count
         nnqs.nnqs_ham_from_pauli([[1, 0]], [[1, 0]], [0.3], 2, device=-1)
     assert e.value.code == nnqs.NNQS_E_ODD_Y
+
+
+def test_options_layout_and_defaults(lib_path):
+    """nnqs_options as the header declares it (16 int32: algorithm, three thresholds,
+    literal_kernel, 11 reserved) and the library defaults the binding relies on."""
+    from paper_2306_16705_b200 import nnqs
+    assert ctypes.sizeof(nnqs.Options) == 64
+    src = open(HDR).read()
+    for name in ("NNQS_LIT_AUTO 0", "NNQS_LIT_STAGED 1", "NNQS_LIT_PLAIN 2", "int32_t literal_kernel;",
+                 "int32_t reserved[11];"):
+        assert name in src, name
+    o = nnqs.nnqs_options_default()
+    assert (o.algorithm, o.literal_kernel) == (0, 0)
+    assert (o.thr_single, o.thr_double, o.thr_rowheavy) == (128, 8192, 16384)
+    assert list(o.reserved) == [0] * 11
