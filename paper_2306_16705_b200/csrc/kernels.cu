@@ -542,20 +542,30 @@ struct __align__(16) BsWarp {
     uint16_t fq[BS_FQ];         // in-sector pairs of a batch in (group, row) order: group | row << 8
 };
 
-// Algorithm 2's lookup of x' (the probe above) with the common case -- an absent key
-// whose first bucket has an empty slot and no fingerprint match -- decided from one
-// 32-B load without a loop
+// Algorithm 2's lookup of x' (the probe above) with each 32-B bucket decided from one
+// load: the slots whose fingerprint matches are compared with the key; the bucket
+// ends the search unless it is full (slots fill in order, so slot 3 tells)
 __device__ __forceinline__ int64_t probe_fast(const TabView &T, u64 h, u64 p0, u64 p1) {
-    const u64 b = h & T.bucket_mask;
+    u64 b = h & T.bucket_mask;
     const uint32_t fp = (uint32_t)(h >> 32);
-    const ulonglong2 *bk = reinterpret_cast<const ulonglong2 *>(T.slots + 4 * b);
-    const ulonglong2 s01 = __ldg(bk), s23 = __ldg(bk + 1);
-    const bool m0 = (uint32_t)(s01.x >> 32) == fp && s01.x != NNQS_EMPTY_SLOT;
-    const bool m1 = (uint32_t)(s01.y >> 32) == fp && s01.y != NNQS_EMPTY_SLOT;
-    const bool m2 = (uint32_t)(s23.x >> 32) == fp && s23.x != NNQS_EMPTY_SLOT;
-    const bool m3 = (uint32_t)(s23.y >> 32) == fp && s23.y != NNQS_EMPTY_SLOT;
-    if (!(m0 | m1 | m2 | m3) && s23.y == NNQS_EMPTY_SLOT) return -1;   // slots fill in order
-    return probe(T, h, p0, p1);
+    while (true) {
+        const ulonglong2 *bk = reinterpret_cast<const ulonglong2 *>(T.slots + 4 * b);
+        const ulonglong2 s01 = __ldg(bk), s23 = __ldg(bk + 1);
+        const u64 sl[4] = {s01.x, s01.y, s23.x, s23.y};
+        unsigned m = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            m |= (unsigned)((uint32_t)(sl[i] >> 32) == fp && sl[i] != NNQS_EMPTY_SLOT) << i;
+        while (m) {
+            const int i = __ffs(m) - 1;
+            m &= m - 1;
+            const uint32_t r = (uint32_t)(i == 0 ? s01.x : i == 1 ? s01.y : i == 2 ? s23.x : s23.y);
+            const ulonglong2 k = __ldg(T.keys + r);
+            if (k.x == p0 && k.y == p1) return (int64_t)r;
+        }
+        if (s23.y == NNQS_EMPTY_SLOT) return -1;
+        b = (b + 1) & T.bucket_mask;
+    }
 }
 
 __device__ __forceinline__ uint32_t ffilt(u64 w, int base) {
@@ -1069,7 +1079,7 @@ int nnqs_table_build(nnqs_table t, const uint64_t *keys, const double *logpsi, v
     t->bytes = 16 + 2 * (int64_t)bk;
     if (t->mode == 0) {
         u64 nb = 1;
-        while (nb * 4 < 2 * (u64)(n > 0 ? n : 1)) nb <<= 1;   // load factor <= 1/2
+        while (nb * 4 < 4 * (u64)(n > 0 ? n : 1)) nb <<= 1;   // load factor <= 1/4: ~2 % of buckets full
         t->bucket_mask = nb - 1;
         if ((rc = cuda_check(nnqs_malloc_async(&t->keys, bk ? bk : 16, st), "alloc keys"))) return rc;
         if ((rc = cuda_check(nnqs_malloc_async((void **)&t->slots, 32 * nb, st), "alloc slots"))) return rc;
