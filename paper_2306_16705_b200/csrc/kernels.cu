@@ -568,6 +568,27 @@ __device__ __forceinline__ int64_t probe_fast(const TabView &T, u64 h, u64 p0, u
     }
 }
 
+// probe_fast with the first bucket's 32 B already loaded (s01, s23)
+__device__ __forceinline__ int64_t probe_resolve(const TabView &T, u64 h, u64 p0, u64 p1, ulonglong2 s01,
+                                                 ulonglong2 s23) {
+    const uint32_t fp = (uint32_t)(h >> 32);
+    const u64 sl[4] = {s01.x, s01.y, s23.x, s23.y};
+    unsigned m = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) m |= (unsigned)((uint32_t)(sl[i] >> 32) == fp && sl[i] != NNQS_EMPTY_SLOT) << i;
+    while (m) {
+        const int i = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t r = (uint32_t)(i == 0 ? s01.x : i == 1 ? s01.y : i == 2 ? s23.x : s23.y);
+        const ulonglong2 k = __ldg(T.keys + r);
+        if (k.x == p0 && k.y == p1) return (int64_t)r;
+    }
+    if (s23.y == NNQS_EMPTY_SLOT) return -1;
+    // full bucket: continue with the next one (the same walk as probe_fast)
+    const u64 h2 = (h & ~T.bucket_mask) | ((h + 1) & T.bucket_mask);
+    return probe_fast(T, h2, p0, p1);
+}
+
 __device__ __forceinline__ uint32_t ffilt(u64 w, int base) {
     uint32_t f = 0;
     while (w) {
@@ -728,71 +749,94 @@ __global__ void __launch_bounds__(BS_WARPS * 32, 1) k_eloc_bs(HamView H, const B
                     }
                     __syncwarp();
                     const int lim = min(total, base + BS_FQ);
-                    for (int f0 = base; f0 < lim; f0 += 32) {
-                        const int f = f0 + lane;
-                        int64_t idx = -1;
-                        int row = 0, lo = 0;
-                        if (f < lim) {
-                            const uint32_t e = W.fq[f - base];
-                            lo = (int)(e & 0xff);
-                            row = (int)(e >> 8);
-                            const uint4 rh = W.rh[row];
-                            const BsRec &G = tl[g0 + lo];
-                            if (bm_test(bmA, rh.z ^ G.fa) && bm_test(bmB, rh.w ^ G.fb)) {
-                                const ulonglong2 xr = W.rx[row];
-                                const ulonglong2 X = G.x;
-                                const u64 hxr = (u64)rh.x | ((u64)rh.y << 32);
-                                idx = probe_fast(T, hxr ^ G.hx, xr.x ^ X.x, xr.y ^ X.y);
-                            }
-                        }
+                    // a pair's lookup: the filter, then its first bucket (the load is issued for
+                    // two pairs per lane before either is resolved: two lookups in flight)
+                    auto prep = [&](int f, int &lo, int &row, u64 &h, u64 &p0, u64 &p1) -> bool {
+                        if (f >= lim) return false;
+                        const uint32_t e = W.fq[f - base];
+                        lo = (int)(e & 0xff);
+                        row = (int)(e >> 8);
+                        const uint4 rh = W.rh[row];
+                        const BsRec &G = tl[g0 + lo];
+                        if (!(bm_test(bmA, rh.z ^ G.fa) && bm_test(bmB, rh.w ^ G.fb))) return false;
+                        const ulonglong2 xr = W.rx[row];
+                        const ulonglong2 X = G.x;
+                        h = ((u64)rh.x | ((u64)rh.y << 32)) ^ G.hx;
+                        p0 = xr.x ^ X.x;
+                        p1 = xr.y ^ X.y;
+                        return true;
+                    };
+                    // a round's hits: H_xx' and psi(x')/psi-hat by the finding lane, then each
+                    // row's lane adds its hits in (group) order
+                    auto apply = [&](int64_t idx, int lo, int row) {
                         const unsigned hm = __ballot_sync(FULL, idx >= 0);
-                        if (hm) {                            // rare: ~0.4 hits per 32 x 32 pairs at C5
-                            if (idx >= 0) {                  // H_xx': the group's strings in order
-                                const BsRec &G = tl[g0 + lo];
-                                const ulonglong2 xr = W.rx[row];
-                                const uint32_t b = G.sb, e = G.se & 0x7FFFFFFFu;
-                                double hv = 0.0;
-                                for (uint32_t i = b; i < e; ++i) {
-                                    const ulonglong2 Z = __ldg(H.tz + i);
-                                    const int par = (__popcll(xr.x & Z.x) + __popcll(xr.y & Z.y)) & 1;
-                                    hv += flip_sign(__ldg(H.td + i), par);
-                                }
-                                c_str += e - b;
-                                const double2 lr = W.rl[row];
-                                double2 ps;
-                                if (!((lr.x - s) < -600.0)) {
-                                    ps = __ldg(T.psi_hat + idx);
-                                } else {                     // reading R11
-                                    const double2 l2 = T.logpsi[idx];
-                                    const double mm = exp(l2.x - lr.x);
-                                    double sn, cs2;
-                                    sincos(l2.y - lr.y, &sn, &cs2);
-                                    ps = make_double2(mm * cs2, mm * sn);
-                                }
-                                W.qh[lane] = hv;
-                                W.qp[lane] = ps;
-                                W.qr[lane] = row;
+                        if (!hm) return;                     // rare: ~0.4 hits per 32 x 32 pairs at C5
+                        if (idx >= 0) {                      // H_xx': the group's strings in order
+                            const BsRec &G = tl[g0 + lo];
+                            const ulonglong2 xr = W.rx[row];
+                            const uint32_t b = G.sb, e = G.se & 0x7FFFFFFFu;
+                            double hv = 0.0;
+                            for (uint32_t i = b; i < e; ++i) {
+                                const ulonglong2 Z = __ldg(H.tz + i);
+                                const int par = (__popcll(xr.x & Z.x) + __popcll(xr.y & Z.y)) & 1;
+                                hv += flip_sign(__ldg(H.td + i), par);
                             }
-                            __syncwarp();
-                            unsigned h2 = hm;                // each row adds its hits in (group) order
-                            while (h2) {
-                                const int l = __ffs(h2) - 1;
-                                h2 &= h2 - 1;
-                                const int rw = W.qr[l];
-                                if ((rw & 31) == lane) {
-                                    const double hv = W.qh[l];
-                                    const double2 ps = W.qp[l];
-    #pragma unroll
-                                    for (int p = 0; p < NP; ++p) {
-                                        if ((rw >> 5) != p) continue;
-                                        ar[p] = fma(hv, ps.x, ar[p]);
-                                        ai[p] = fma(hv, ps.y, ai[p]);
-                                    }
-                                    ++c_hit;
-                                }
+                            c_str += e - b;
+                            const double2 lr = W.rl[row];
+                            double2 ps;
+                            if (!((lr.x - s) < -600.0)) {
+                                ps = __ldg(T.psi_hat + idx);
+                            } else {                         // reading R11
+                                const double2 l2 = T.logpsi[idx];
+                                const double mm = exp(l2.x - lr.x);
+                                double sn, cs2;
+                                sincos(l2.y - lr.y, &sn, &cs2);
+                                ps = make_double2(mm * cs2, mm * sn);
                             }
-                            __syncwarp();
+                            W.qh[lane] = hv;
+                            W.qp[lane] = ps;
+                            W.qr[lane] = row;
                         }
+                        __syncwarp();
+                        unsigned h2 = hm;
+                        while (h2) {
+                            const int l = __ffs(h2) - 1;
+                            h2 &= h2 - 1;
+                            const int rw = W.qr[l];
+                            if ((rw & 31) == lane) {
+                                const double hv = W.qh[l];
+                                const double2 ps = W.qp[l];
+#pragma unroll
+                                for (int p = 0; p < NP; ++p) {
+                                    if ((rw >> 5) != p) continue;
+                                    ar[p] = fma(hv, ps.x, ar[p]);
+                                    ai[p] = fma(hv, ps.y, ai[p]);
+                                }
+                                ++c_hit;
+                            }
+                        }
+                        __syncwarp();
+                    };
+                    for (int f0 = base; f0 < lim; f0 += 64) {
+                        int loA = 0, rowA = 0, loB = 0, rowB = 0;
+                        u64 hA = 0, aA0 = 0, aA1 = 0, hB = 0, aB0 = 0, aB1 = 0;
+                        const bool wA = prep(f0 + lane, loA, rowA, hA, aA0, aA1);
+                        const bool wB = prep(f0 + 32 + lane, loB, rowB, hB, aB0, aB1);
+                        ulonglong2 sA01, sA23, sB01, sB23;
+                        if (wA) {
+                            const ulonglong2 *bk = reinterpret_cast<const ulonglong2 *>(T.slots + 4 * (hA & T.bucket_mask));
+                            sA01 = __ldg(bk);
+                            sA23 = __ldg(bk + 1);
+                        }
+                        if (wB) {
+                            const ulonglong2 *bk = reinterpret_cast<const ulonglong2 *>(T.slots + 4 * (hB & T.bucket_mask));
+                            sB01 = __ldg(bk);
+                            sB23 = __ldg(bk + 1);
+                        }
+                        const int64_t idxA = wA ? probe_resolve(T, hA, aA0, aA1, sA01, sA23) : -1;
+                        const int64_t idxB = wB ? probe_resolve(T, hB, aB0, aB1, sB01, sB23) : -1;
+                        apply(idxA, loA, rowA);              // (group, row) order: the first 32 pairs,
+                        apply(idxB, loB, rowB);              // then the next 32
                     }
                     __syncwarp();                        // the queue is refilled by the next pass / batch
                 }
