@@ -285,8 +285,10 @@ int nnqs_table_prepare_ex(nnqs_ham h, int mode, const uint64_t *keys, const doub
     if (!rc && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
         rc = nnqs_set_error(NNQS_E_CUDA, "cudaEventCreate failed");
     t->last_use = ev;
-    if (!rc) rc = nnqs_table_build(t, keys, logpsi, cuda_stream);
-    if (!rc && mode == 0) rc = nnqs_table_build_spin(h, t, cuda_stream);
+    bool checked = false;   // the order / exp-ratio flags are read at the spin build's first sync
+    if (!rc) rc = nnqs_table_build(t, keys, logpsi, cuda_stream, /*defer_check=*/mode == 0);
+    if (!rc && mode == 0) rc = nnqs_table_build_spin(h, t, cuda_stream, &checked);
+    if (!rc && mode == 0 && !checked && n) rc = nnqs_table_check(t, nullptr, cuda_stream);
     if (!rc) cudaEventRecord((cudaEvent_t)t->last_use, (cudaStream_t)cuda_stream);
     if (rc) {
         cudaStreamSynchronize((cudaStream_t)cuda_stream);

@@ -181,7 +181,8 @@ struct nnqs_table_s {
     int n_heavy = 0;
 };
 
-int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream);
+// checked: set when the spin build has read and checked the table flags (nnqs_table_check)
+int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream, bool *checked);
 void nnqs_table_release_spin(nnqs_table t);
 // fused first pass of Eq. (6) per chunk of NNQS_REDUCE_CHUNK rows (nnqs_local_energy's
 // counts / partials_out): ctr = device u32[n_chunks] zeroed by the caller
@@ -205,7 +206,10 @@ int nnqs_chunk_work_spin(nnqs_table t, int64_t chunk, int64_t *work_host, int64_
 // device side (kernels.cu)
 int nnqs_ham_upload(nnqs_ham h);
 void nnqs_ham_release(nnqs_ham h);
-int nnqs_table_build(nnqs_table t, const uint64_t *keys, const double *logpsi, void *stream);
+// defer_check: leave the read of the order / exp-ratio flags (a host sync) to the caller,
+// which must then call nnqs_table_check (nnqs_table_build_spin folds it into its first sync)
+int nnqs_table_build(nnqs_table t, const uint64_t *keys, const double *logpsi, void *stream, bool defer_check);
+int nnqs_table_check(nnqs_table t, const int *host_flags, void *stream);
 void nnqs_table_release(nnqs_table t);
 int nnqs_launch_local_energy(nnqs_ham h, nnqs_table t, int64_t row_begin, const uint64_t *rows,
                              const double *row_logpsi, int64_t n_rows, double *eloc,

@@ -895,14 +895,27 @@ __global__ void __launch_bounds__(BS_WARPS * 32, 1) k_eloc_bs(HamView H, const B
 
 // per-spin string filter bitmaps of a mode-0 table (k_eloc_bs): bit f_alpha(key) and bit f_beta(key)
 __global__ void k_bs_bitmap(const ulonglong2 *keys, int64_t n, uint32_t *bm) {
+    __shared__ uint32_t col[128];                   // the filter columns (per-lane bit loops: no
+    if (threadIdx.x < 128) col[threadIdx.x] = c_filt[threadIdx.x];   // serialised constant reads)
+    __syncthreads();
+    auto f = [&](u64 w, int base) {
+        uint32_t v = 0;
+        while (w) {
+            v ^= col[base + __ffsll((long long)w) - 1];
+            w &= w - 1;
+        }
+        return v;
+    };
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const ulonglong2 k = keys[i];
-        const uint32_t fa = ffilt(k.x & ALPHA_MASK, 0) ^ ffilt(k.y & ALPHA_MASK, 64);
-        const uint32_t fb = ffilt(k.x & BETA_MASK, 0) ^ ffilt(k.y & BETA_MASK, 64);
+        const uint32_t fa = f(k.x & ALPHA_MASK, 0) ^ f(k.y & ALPHA_MASK, 64);
+        const uint32_t fb = f(k.x & BETA_MASK, 0) ^ f(k.y & BETA_MASK, 64);
         const uint32_t ba = fa & ((1u << BS_FB) - 1), bb = fb & ((1u << BS_FB) - 1);
-        atomicOr(bm + (ba >> 5), 1u << (ba & 31));
-        atomicOr(bm + BS_BM_WORDS / 2 + (bb >> 5), 1u << (bb & 31));
+        // most keys share their alpha or beta string with many others: read before the atomic
+        if (!(__ldcg(bm + (ba >> 5)) >> (ba & 31) & 1u)) atomicOr(bm + (ba >> 5), 1u << (ba & 31));
+        if (!(__ldcg(bm + BS_BM_WORDS / 2 + (bb >> 5)) >> (bb & 31) & 1u))
+            atomicOr(bm + BS_BM_WORDS / 2 + (bb >> 5), 1u << (bb & 31));
     }
 }
 
@@ -1105,7 +1118,7 @@ void nnqs_ham_release(nnqs_ham h) {
     D = DeviceHam();
 }
 
-int nnqs_table_build(nnqs_table t, const uint64_t *keys, const double *logpsi, void *stream) {
+int nnqs_table_build(nnqs_table t, const uint64_t *keys, const double *logpsi, void *stream, bool defer_check) {
     int rc = ensure_hash(t->device);
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
@@ -1145,13 +1158,23 @@ int nnqs_table_build(nnqs_table t, const uint64_t *keys, const double *logpsi, v
                                                      (double2 *)t->psi_hat, t->flag + 1);
     }
     if ((rc = cuda_check(cudaGetLastError(), "table kernels"))) return rc;
-    if (n) {
-        int flag[2] = {0, 0};   // order violation, rows with psi_hat(x) < e^-600
+    if (n && !defer_check) return nnqs_table_check(t, nullptr, stream);
+    return NNQS_OK;
+}
+
+// the build's flags (order violation, rows on the exp-ratio path): read with a sync of
+// `stream`, or (host != nullptr) already copied there by a caller that synchronised
+int nnqs_table_check(nnqs_table t, const int *host, void *stream) {
+    int flag[2] = {0, 0};   // order violation, rows with psi_hat(x) < e^-600
+    if (!host) {
+        cudaStream_t st = (cudaStream_t)stream;
+        int rc;
         if ((rc = cuda_check(cudaMemcpyAsync(flag, t->flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, st), "read flag"))) return rc;
         if ((rc = cuda_check(cudaStreamSynchronize(st), "sync"))) return rc;
-        t->n_direct = flag[1];
-        if (t->mode == 0 && flag[0]) return nnqs_set_error(NNQS_E_TABLE, "keys are not strictly increasing as 128-bit integers");
+        host = flag;
     }
+    t->n_direct = host[1];
+    if (t->mode == 0 && host[0]) return nnqs_set_error(NNQS_E_TABLE, "keys are not strictly increasing as 128-bit integers");
     return NNQS_OK;
 }
 

@@ -1718,14 +1718,12 @@ __global__ void __launch_bounds__(256) k_chunk_work(TabSpin T, int64_t chunk, in
     }
 }
 
-__global__ void k_find_heavy(const int32_t *listA_idx, const int32_t *ga_of, const int32_t *offA, int64_t n,
-                             int32_t thr, int32_t *out, int *count) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-         j += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t g = ga_of[listA_idx[j]];
-        if (offA[g] == (int32_t)j && offA[g + 1] - offA[g] > thr) out[atomicAdd(count, 1)] = g;
-    }
-}
+// predicate of the heavy alpha groups (more than thr rows) for cub::DeviceSelect::If
+struct HeavyGroup {
+    const int32_t *offA;
+    int32_t thr;
+    __device__ __forceinline__ bool operator()(const int32_t g) const { return offA[g + 1] - offA[g] > thr; }
+};
 
 }  // namespace
 
@@ -2252,7 +2250,7 @@ int build_multimap(nnqs_table t, int64_t n, cudaStream_t st, int32_t *counts, vo
 }
 }  // namespace
 
-int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
+int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream, bool *checked) {
     if (!h->spin.ok || t->mode != 0 || t->n == 0) return NNQS_OK;
     t->spin_n = h->spin.n;
     cudaStream_t st = (cudaStream_t)stream;
@@ -2319,8 +2317,12 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
             k_csr<<<g, 256, 0, st>>>(k1, perm2, incl, n, t->sb, t->offA, t->ga_of, t->listA_b, t->listA_idx,
                                      t->ah_keys, t->ah_vals, t->ah_mask);
             int32_t nga = 0;
+            int tflag[2] = {0, 0};   // nnqs_table_build's flags, read at the same sync
             rc = cuda_check(cudaMemcpyAsync(&nga, incl + n - 1, 4, cudaMemcpyDeviceToHost, st), "read alpha groups");
+            if (!rc) rc = cuda_check(cudaMemcpyAsync(tflag, t->flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, st), "read flag");
             if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
+            if (!rc) rc = nnqs_table_check(t, tflag, st);
+            if (checked) *checked = true;
             if (rc) { cudaFreeAsync(scratch, st); return rc; }
             t->n_alpha_groups = nga;
         }
@@ -2427,26 +2429,28 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream) {
     t->thr_rowheavy = t->opt.thr_rowheavy;
     if (t->thr_rowheavy < t->thr_single) t->thr_rowheavy = t->thr_single;   // rows must be in the multimap
     {
+        // heavy alpha groups (more than thr_rowheavy rows) in ascending id order, written
+        // on the device: one read of their count (at most n / (thr_rowheavy + 1) of them)
         int *cnt_d = (int *)incl;   // scratch reuse
-        int32_t *hg = (int32_t *)perm1;
-        cudaMemsetAsync(cnt_d, 0, sizeof(int), st);
-        k_find_heavy<<<g, 256, 0, st>>>(t->listA_idx, t->ga_of, t->offA, n, t->thr_rowheavy, hg, cnt_d);
+        const int cap = (int)std::min<int64_t>(t->n_alpha_groups, n / ((int64_t)t->thr_rowheavy + 1) + 1);
+        rc = cuda_check(nnqs_malloc_async((void **)&t->heavy_groups, 4 * (size_t)std::max(cap, 1), st), "alloc heavy");
+        if (rc) { cudaFreeAsync(scratch, st); return rc; }
+        const HeavyGroup pred{t->offA, t->thr_rowheavy};
+        const int ng = (int)t->n_alpha_groups;
+        size_t tsel = 0;
+        cub::DeviceSelect::If(nullptr, tsel, cub::CountingInputIterator<int32_t>(0), t->heavy_groups, cnt_d, ng, pred, st);
+        void *tmp_sel = nullptr;
+        rc = cuda_check(nnqs_malloc_async(&tmp_sel, std::max<size_t>(tsel, 16), st), "alloc heavy select");
+        if (rc) { cudaFreeAsync(scratch, st); return rc; }
+        cub::DeviceSelect::If(tmp_sel, tsel, cub::CountingInputIterator<int32_t>(0), t->heavy_groups, cnt_d, ng, pred,
+                              st);
+        cudaFreeAsync(tmp_sel, st);
         int nh = 0;
         rc = cuda_check(cudaMemcpyAsync(&nh, cnt_d, sizeof(int), cudaMemcpyDeviceToHost, st), "read heavy");
         if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
         if (rc) { cudaFreeAsync(scratch, st); return rc; }
+        if (nh > cap) { cudaFreeAsync(scratch, st); return nnqs_set_error(NNQS_E_TABLE, "internal: heavy group bound"); }
         t->n_heavy = nh;
-        if (nh) {
-            rc = cuda_check(nnqs_malloc_async((void **)&t->heavy_groups, 4 * nh, st), "alloc heavy");
-            if (rc) { cudaFreeAsync(scratch, st); return rc; }
-            // deterministic order of the heavy groups: sort the few ids on the host
-            std::vector<int32_t> ids(nh);
-            cudaMemcpyAsync(ids.data(), hg, 4 * nh, cudaMemcpyDeviceToHost, st);
-            cudaStreamSynchronize(st);
-            std::sort(ids.begin(), ids.end());
-            cudaMemcpyAsync(t->heavy_groups, ids.data(), 4 * nh, cudaMemcpyHostToDevice, st);
-            cudaStreamSynchronize(st);
-        }
     }
     cudaFreeAsync(scratch, st);
     rc = cuda_check(cudaGetLastError(), "spin index kernels");
