@@ -510,6 +510,9 @@ __global__ void __launch_bounds__(LIT_THREADS, 1) k_eloc_lit(HamView H, const Li
 #ifndef BS_STAGES
 #define BS_STAGES 3
 #endif
+#ifndef BS_LF
+#define BS_LF 2                                   // lookups in flight per lane
+#endif
 #ifndef BS_FQ
 #define BS_FQ 512                                 // pair-queue entries per warp (a batch has <= 32 x 32 BS_P)
 #endif
@@ -749,8 +752,8 @@ __global__ void __launch_bounds__(BS_WARPS * 32, 1) k_eloc_bs(HamView H, const B
                     }
                     __syncwarp();
                     const int lim = min(total, base + BS_FQ);
-                    // a pair's lookup: the filter, then its first bucket (the load is issued for
-                    // two pairs per lane before either is resolved: two lookups in flight)
+                    // a pair's lookup: the filter, then its first bucket (the loads are issued for
+                    // BS_LF pairs per lane before any is resolved: BS_LF lookups in flight)
                     auto prep = [&](int f, int &lo, int &row, u64 &h, u64 &p0, u64 &p1) -> bool {
                         if (f >= lim) return false;
                         const uint32_t e = W.fq[f - base];
@@ -817,26 +820,31 @@ __global__ void __launch_bounds__(BS_WARPS * 32, 1) k_eloc_bs(HamView H, const B
                         }
                         __syncwarp();
                     };
-                    for (int f0 = base; f0 < lim; f0 += 64) {
-                        int loA = 0, rowA = 0, loB = 0, rowB = 0;
-                        u64 hA = 0, aA0 = 0, aA1 = 0, hB = 0, aB0 = 0, aB1 = 0;
-                        const bool wA = prep(f0 + lane, loA, rowA, hA, aA0, aA1);
-                        const bool wB = prep(f0 + 32 + lane, loB, rowB, hB, aB0, aB1);
-                        ulonglong2 sA01, sA23, sB01, sB23;
-                        if (wA) {
-                            const ulonglong2 *bk = reinterpret_cast<const ulonglong2 *>(T.slots + 4 * (hA & T.bucket_mask));
-                            sA01 = __ldg(bk);
-                            sA23 = __ldg(bk + 1);
+                    for (int f0 = base; f0 < lim; f0 += 32 * BS_LF) {
+                        int lo[BS_LF], rw[BS_LF];
+                        u64 hh[BS_LF], a0[BS_LF], a1[BS_LF];
+                        bool w[BS_LF];
+                        ulonglong2 s01[BS_LF], s23[BS_LF];
+                        int64_t idx[BS_LF];
+#pragma unroll
+                        for (int u = 0; u < BS_LF; ++u) {
+                            lo[u] = rw[u] = 0;
+                            hh[u] = a0[u] = a1[u] = 0;
+                            w[u] = prep(f0 + 32 * u + lane, lo[u], rw[u], hh[u], a0[u], a1[u]);
                         }
-                        if (wB) {
-                            const ulonglong2 *bk = reinterpret_cast<const ulonglong2 *>(T.slots + 4 * (hB & T.bucket_mask));
-                            sB01 = __ldg(bk);
-                            sB23 = __ldg(bk + 1);
-                        }
-                        const int64_t idxA = wA ? probe_resolve(T, hA, aA0, aA1, sA01, sA23) : -1;
-                        const int64_t idxB = wB ? probe_resolve(T, hB, aB0, aB1, sB01, sB23) : -1;
-                        apply(idxA, loA, rowA);              // (group, row) order: the first 32 pairs,
-                        apply(idxB, loB, rowB);              // then the next 32
+#pragma unroll
+                        for (int u = 0; u < BS_LF; ++u)
+                            if (w[u]) {
+                                const ulonglong2 *bk =
+                                    reinterpret_cast<const ulonglong2 *>(T.slots + 4 * (hh[u] & T.bucket_mask));
+                                s01[u] = __ldg(bk);
+                                s23[u] = __ldg(bk + 1);
+                            }
+#pragma unroll
+                        for (int u = 0; u < BS_LF; ++u)
+                            idx[u] = w[u] ? probe_resolve(T, hh[u], a0[u], a1[u], s01[u], s23[u]) : -1;
+#pragma unroll
+                        for (int u = 0; u < BS_LF; ++u) apply(idx[u], lo[u], rw[u]);   // (group, row) order
                     }
                     __syncwarp();                        // the queue is refilled by the next pass / batch
                 }
