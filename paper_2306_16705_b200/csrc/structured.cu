@@ -1686,7 +1686,10 @@ __global__ void k_row_cost(TabSpin T, int64_t row_begin, int64_t n_rows, int32_t
         // common heavy a' repeat the same (a', b - e_r) probes, which then hit in L2
         // (measured: 45.2 -> 44.2 ms per C5 call; exact longest-first or pure beta order: 45.1)
         const uint32_t c = la > thr_rowheavy ? 0u : (uint32_t)nl_cost[ga];
-        const uint32_t cls = c ? (uint32_t)((31 - __clz(c)) >> 1) + 1u : 0u;
+#ifndef NNQS_P3_CLASS
+#define NNQS_P3_CLASS 2                           // octaves per cost class
+#endif
+        const uint32_t cls = c ? (uint32_t)((31 - __clz(c)) / NNQS_P3_CLASS) + 1u : 0u;
         c24[r] = (cls << 22) | ((uint32_t)gb & 0x3FFFFFu);
         iota[r] = (int32_t)r;
     }
