@@ -513,6 +513,9 @@ __device__ unsigned long long g_prof[16];
 #define NNQS_PHASE_MASK 15
 #endif
 #define WARPS_PER_BLOCK 8
+#ifndef NNQS_P3_MINB
+#define NNQS_P3_MINB 4   // CTAs per SM of the phase-(iii) kernel (launch bounds)
+#endif
 #ifndef NNQS_AB
 #define NNQS_AB 1      // alpha x beta groups in closed form (SpinIndex::ab_ok)
 #endif
@@ -2694,11 +2697,11 @@ int nnqs_launch_local_energy_spin(nnqs_ham h, nnqs_table t, int64_t row_begin, i
     }
     if (!rc) {
         if (lg_on) {
-            launch(k_eloc_spin<24, 4, false, true>, perm24, st);
-            if (t->n_direct) launch(k_eloc_spin<24, 4, true, true>, perm24, st);
+            launch(k_eloc_spin<24, NNQS_P3_MINB, false, true>, perm24, st);
+            if (t->n_direct) launch(k_eloc_spin<24, NNQS_P3_MINB, true, true>, perm24, st);
         } else {
-            launch(k_eloc_spin<24, 4, false, false>, perm24, st);
-            if (t->n_direct) launch(k_eloc_spin<24, 4, true, false>, perm24, st);
+            launch(k_eloc_spin<24, NNQS_P3_MINB, false, false>, perm24, st);
+            if (t->n_direct) launch(k_eloc_spin<24, NNQS_P3_MINB, true, false>, perm24, st);
         }
     }
     return cleanup(rc);
