@@ -22,6 +22,7 @@
 // slicing / number of GPUs.
 #include <cuda_runtime.h>
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <mutex>
@@ -2450,11 +2451,11 @@ int nnqs_table_build_spin(nnqs_ham h, nnqs_table t, void *stream, bool *checked)
         const HeavyGroup pred{t->offA, t->thr_rowheavy};
         const int ng = (int)t->n_alpha_groups;
         size_t tsel = 0;
-        cub::DeviceSelect::If(nullptr, tsel, cub::CountingInputIterator<int32_t>(0), t->heavy_groups, cnt_d, ng, pred, st);
+        cub::DeviceSelect::If(nullptr, tsel, thrust::counting_iterator<int32_t>(0), t->heavy_groups, cnt_d, ng, pred, st);
         void *tmp_sel = nullptr;
         rc = cuda_check(nnqs_malloc_async(&tmp_sel, std::max<size_t>(tsel, 16), st), "alloc heavy select");
         if (rc) { cudaFreeAsync(scratch, st); return rc; }
-        cub::DeviceSelect::If(tmp_sel, tsel, cub::CountingInputIterator<int32_t>(0), t->heavy_groups, cnt_d, ng, pred,
+        cub::DeviceSelect::If(tmp_sel, tsel, thrust::counting_iterator<int32_t>(0), t->heavy_groups, cnt_d, ng, pred,
                               st);
         cudaFreeAsync(tmp_sel, st);
         int nh = 0;
